@@ -1,0 +1,164 @@
+"""Thin Python binding over the C-ABI (include/cbvh.h): argument marshalling only.
+
+Every step of the hot path runs in libcbvh.so (host builder in C++, traversal
+and leaf tests in sm_100a CUDA kernels).  PyTorch supplies device memory and
+streams.  Names follow the C-ABI: build_compressed_bvh, collide_batch,
+distance_batch.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class CompressedBVH:
+    """A host blob (numpy uint8) plus, after ``to_device``, its bound device copy."""
+
+    blob: np.ndarray
+    info: dict
+    device_blob: object = None  # torch.uint8 tensor on the GPU
+    bound: L.cbvh_bvh = None
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.blob.nbytes)
+
+    def to_device(self, device="cuda") -> "CompressedBVH":
+        torch = _torch()
+        d = torch.from_numpy(self.blob).to(device)
+        if d.data_ptr() % 256:
+            raise RuntimeError("device blob not 256-byte aligned")
+        b = L.cbvh_bvh()
+        L.check(L.load().cbvh_bind(self.blob.ctypes.data_as(C.POINTER(C.c_uint8)), self.blob.nbytes,
+                                   C.c_void_p(d.data_ptr()), C.byref(b)))
+        self.device_blob, self.bound = d, b
+        return self
+
+
+def blob_info(blob: np.ndarray) -> dict:
+    info = L.cbvh_info()
+    b = np.ascontiguousarray(blob, dtype=np.uint8)
+    L.check(L.load().cbvh_blob_info(b.ctypes.data_as(C.POINTER(C.c_uint8)), b.nbytes, C.byref(info)))
+    h = info.h
+    return dict(branching=h.branching, bits=h.bits, treelet_nodes=h.treelet_nodes, leaf_size=h.leaf_size,
+                code_width=h.code_width, num_nodes=h.num_nodes, num_tris=h.num_tris,
+                num_treelets=h.num_treelets, depth=h.depth, num_leaves=h.num_leaves,
+                lattice_exp=h.lattice_exp, origin=tuple(h.origin), root_box=tuple(h.root_box),
+                off_topo=h.off_topo, off_codes=h.off_codes, off_treelets=h.off_treelets,
+                off_tris=h.off_tris, off_tri_index=h.off_tri_index, total_bytes=h.total_bytes,
+                bvh_bytes=info.bvh_bytes, tri_bytes=info.tri_bytes, bytes_per_node=info.bytes_per_node,
+                code_bytes_per_node=info.code_bytes_per_node)
+
+
+def build_compressed_bvh(vertices, triangles, branching: int = 4, bits: int = 8,
+                         treelet_nodes: int = 32, leaf_size: int = 4) -> CompressedBVH:
+    """C-ABI build_compressed_bvh: host BVH build, lattice quantization,
+    predictor–corrector codes and treelet packing."""
+    lib = L.load()
+    v = np.ascontiguousarray(vertices, dtype=np.float32).reshape(-1, 3)
+    t = np.ascontiguousarray(triangles, dtype=np.int32).reshape(-1, 3)
+    mesh = L.cbvh_mesh(v.ctypes.data_as(C.POINTER(C.c_float)), len(v),
+                       t.ctypes.data_as(C.POINTER(C.c_int32)), len(t))
+    opts = L.cbvh_build_opts(int(treelet_nodes), int(leaf_size))
+    out = C.POINTER(C.c_uint8)()
+    n = C.c_size_t(0)
+    L.check(lib.build_compressed_bvh(C.byref(mesh), int(branching), int(bits), C.byref(opts),
+                                     C.byref(out), C.byref(n)))
+    try:
+        blob = np.ctypeslib.as_array(out, shape=(n.value,)).copy()
+    finally:
+        lib.cbvh_free_blob(out)
+    return CompressedBVH(blob=blob, info=blob_info(blob))
+
+
+class Workspace:
+    """Device workspace (control words, stats, per-warp stack spill areas)."""
+
+    def __init__(self, A: CompressedBVH, B: CompressedBVH, mode: int = 0, device="cuda"):
+        torch = _torch()
+        nb = L.load().cbvh_workspace_bytes(C.byref(A.bound), C.byref(B.bound), 0, int(mode))
+        if nb == 0:
+            raise L.CbvhError(L.CBVH_ECUDA, "cbvh_workspace_bytes failed: "
+                              + L.load().cbvh_last_error().decode(errors="replace"))
+        self.nbytes = int(nb)
+        self.tensor = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+        assert self.tensor.data_ptr() % 256 == 0
+
+    @property
+    def ptr(self) -> int:
+        return self.tensor.data_ptr()
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def _check_poses(poses):
+    torch = _torch()
+    if not (isinstance(poses, torch.Tensor) and poses.is_cuda and poses.dtype == torch.float32):
+        raise TypeError("poses must be a CUDA float32 tensor [N, 12]")
+    if poses.dim() != 2 or poses.shape[1] != 12 or not poses.is_contiguous():
+        raise ValueError("poses must be contiguous [N, 12] row-major [R|t]")
+    return int(poses.shape[0])
+
+
+def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=None,
+                  workspace: Workspace | None = None, stream=None, stats: bool = False):
+    """C-ABI collide_batch: per-pose hit flag (uint8) and colliding pair count (int32 view of uint32)."""
+    torch = _torch()
+    N = _check_poses(poses)
+    dev = poses.device
+    if hit is None:
+        hit = torch.empty(N, dtype=torch.uint8, device=dev)
+    if count is None:
+        count = torch.empty(N, dtype=torch.int32, device=dev)
+    if workspace is None:
+        workspace = Workspace(A, B, 0, dev)
+    f = L.load().collide_batch_stats if stats else L.load().collide_batch
+    L.check(f(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
+              C.c_void_p(hit.data_ptr()), C.c_void_p(count.data_ptr()), C.c_void_p(workspace.ptr),
+              workspace.nbytes, C.c_void_p(_stream_ptr(stream))))
+    return hit, count
+
+
+def distance_batch(A: CompressedBVH, B: CompressedBVH, poses, dist=None,
+                   workspace: Workspace | None = None, stream=None, stats: bool = False):
+    """C-ABI distance_batch: per-pose minimum triangle–triangle distance (fp32)."""
+    torch = _torch()
+    N = _check_poses(poses)
+    if dist is None:
+        dist = torch.empty(N, dtype=torch.float32, device=poses.device)
+    if workspace is None:
+        workspace = Workspace(A, B, 1, poses.device)
+    f = L.load().distance_batch_stats if stats else L.load().distance_batch
+    L.check(f(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
+              C.c_void_p(dist.data_ptr()), C.c_void_p(workspace.ptr), workspace.nbytes,
+              C.c_void_p(_stream_ptr(stream))))
+    return dist
+
+
+def check(workspace: Workspace, stream=None) -> None:
+    """Sync the stream and raise on a device-side error (e.g. stack overflow)."""
+    L.check(L.load().cbvh_check(C.c_void_p(workspace.ptr), C.c_void_p(_stream_ptr(stream))))
+
+
+def read_stats(workspace: Workspace, stream=None) -> dict:
+    s = L.cbvh_stats()
+    L.check(L.load().cbvh_read_stats(C.c_void_p(workspace.ptr), C.byref(s), C.c_void_p(_stream_ptr(stream))))
+    return {k: int(getattr(s, k)) for k, _ in L.cbvh_stats._fields_}
+
+
+def last_launch_count() -> int:
+    return int(L.load().cbvh_last_launch_count())

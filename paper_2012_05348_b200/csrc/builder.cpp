@@ -1,0 +1,398 @@
+// builder.cpp — host-side BVH builder, integer-lattice quantizer,
+// predictor–corrector encoder and treelet packer (BJ subsystem (1)).
+//
+// Paper mapping (P:n = PAPER.md line n, S:n = SPEC.md line n):
+//   * "By splitting the models and wrap it recursively": equal-count
+//     median split on the longest centroid axis, ties by triangle index
+//     (S:178); for B = 4 / 8 the binary median splits are applied
+//     log2(B) times and collapsed into one B-ary node (reading R8).
+//   * "quantify BV as integer" and "predictors based on the delta to
+//     the parent nodes": every box lives on a per-tree power-of-two
+//     integer lattice; a node stores 6 inward b-bit corrections against its
+//     parent's DECODED box, step 2^s with
+//     s = max(0, bitlen(E) - b), E the parent's lattice extent (reading R3).
+//   * "clustering BVHs into a smaller parts ('treelet')": greedy
+//     BFS packing of sibling groups into treelets of at most T nodes; each
+//     treelet header stores the absolute box its first sibling group is coded
+//     against, so any treelet decodes from its own bytes.
+//
+// The blob layout is DESIGN.md §3; the device side reads it in cbvh_device.cu.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/cbvh.h"
+#include "cbvh_internal.h"
+
+namespace cbvh {
+
+namespace {
+
+struct BNode {
+  double lo[3], hi[3];
+  std::vector<int> children;
+  int tri_begin = 0, tri_end = 0;  // range into the permutation (leaves)
+  int depth = 0;
+};
+
+struct Builder {
+  const float* V;
+  const int32_t* T;
+  int64_t nt;
+  int B, c;
+  std::vector<int> perm;
+  std::vector<double> cen;  // centroids [nt*3]
+  std::vector<BNode> nodes;
+
+  double centroid(int t, int a) const { return cen[3 * (size_t)t + a]; }
+
+  void fit(int b, int e, double* lo, double* hi) const {
+    for (int a = 0; a < 3; ++a) { lo[a] = INFINITY; hi[a] = -INFINITY; }
+    for (int k = b; k < e; ++k) {
+      int t = perm[k];
+      for (int v = 0; v < 3; ++v)
+        for (int a = 0; a < 3; ++a) {
+          double x = (double)V[3 * (int64_t)T[3 * (int64_t)t + v] + a];
+          lo[a] = std::min(lo[a], x);
+          hi[a] = std::max(hi[a], x);
+        }
+    }
+  }
+
+  // One binary median split of perm[b, e) on the longest centroid axis.
+  int median_split(int b, int e) {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int k = b; k < e; ++k)
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = std::min(lo[a], centroid(perm[k], a));
+        hi[a] = std::max(hi[a], centroid(perm[k], a));
+      }
+    int ax = 0;
+    for (int a = 1; a < 3; ++a)
+      if (hi[a] - lo[a] > hi[ax] - lo[ax]) ax = a;
+    std::sort(perm.begin() + b, perm.begin() + e, [&](int x, int y) {
+      double cx = centroid(x, ax), cy = centroid(y, ax);
+      return cx < cy || (cx == cy && x < y);
+    });
+    return b + (e - b) / 2;
+  }
+
+  void split(int b, int e, int levels, std::vector<std::pair<int, int>>& out) {
+    if (levels == 0 || e - b <= c) { out.push_back({b, e}); return; }
+    int m = median_split(b, e);
+    split(b, m, levels - 1, out);
+    split(m, e, levels - 1, out);
+  }
+
+  int build(int b, int e, int depth) {
+    int id = (int)nodes.size();
+    nodes.emplace_back();
+    fit(b, e, nodes[id].lo, nodes[id].hi);
+    nodes[id].depth = depth;
+    if (e - b <= c) { nodes[id].tri_begin = b; nodes[id].tri_end = e; return id; }
+    int levels = (B == 2) ? 1 : (B == 4) ? 2 : 3;
+    std::vector<std::pair<int, int>> parts;
+    split(b, e, levels, parts);
+    std::vector<int> ch;
+    for (auto& p : parts) ch.push_back(build(p.first, p.second, depth + 1));
+    nodes[id].children = ch;
+    return id;
+  }
+};
+
+inline int bitlen64(int64_t x) { int n = 0; while (x > 0) { ++n; x >>= 1; } return n; }
+
+template <class X> void put(std::vector<uint8_t>& buf, size_t off, X x) { std::memcpy(&buf[off], &x, sizeof(X)); }
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_opts* opts,
+               std::vector<uint8_t>& out) {
+  if (!mesh) return set_error(CBVH_EINVAL, "mesh is null");
+  if (branching != 2 && branching != 4 && branching != 8) return set_error(CBVH_EINVAL, "branching must be 2, 4 or 8");
+  if (bits < 2 || bits > 16) return set_error(CBVH_EINVAL, "bits must be in [2, 16]");
+  int T = opts ? opts->treelet_nodes : 32;
+  int c = opts ? opts->leaf_size : 4;
+  if (T < branching || T > (1 << 20)) return set_error(CBVH_EINVAL, "treelet_nodes must be >= branching");
+  if (c < 1 || c > 4) return set_error(CBVH_EINVAL, "leaf_size must be in [1, 4]");
+  if (!mesh->vertices || !mesh->triangles) return set_error(CBVH_EINVAL, "null mesh arrays");
+  const int64_t nv = mesh->num_vertices, nt = mesh->num_triangles;
+  if (nt <= 0 || nv <= 0) return set_error(CBVH_EMESH, "empty mesh");
+  if (nt >= (int64_t(1) << 29)) return set_error(CBVH_EMESH, "too many triangles (max 2^29 - 1)");
+  for (int64_t i = 0; i < 3 * nt; ++i)
+    if (mesh->triangles[i] < 0 || mesh->triangles[i] >= nv) return set_error(CBVH_EMESH, "triangle index out of range");
+  for (int64_t i = 0; i < 3 * nv; ++i)
+    if (!std::isfinite(mesh->vertices[i])) return set_error(CBVH_EMESH, "non-finite vertex");
+
+  Builder bd;
+  bd.V = mesh->vertices; bd.T = mesh->triangles; bd.nt = nt; bd.B = branching; bd.c = c;
+  bd.perm.resize(nt);
+  bd.cen.resize(3 * (size_t)nt);
+  for (int64_t t = 0; t < nt; ++t) {
+    bd.perm[t] = (int)t;
+    for (int a = 0; a < 3; ++a) {
+      double s = 0;
+      for (int v = 0; v < 3; ++v) s += (double)mesh->vertices[3 * (int64_t)mesh->triangles[3 * t + v] + a];
+      bd.cen[3 * t + a] = s / 3.0;
+    }
+  }
+  bd.build(0, (int)nt, 0);
+  const int n = (int)bd.nodes.size();
+  if (n >= (1 << 28)) return set_error(CBVH_EMESH, "too many nodes (max 2^28 - 1)");
+
+  // ---- integer lattice (reading R3): origin = root lo (fp32 values), cell 2^e
+  const BNode& root = bd.nodes[0];
+  double ext = 0;
+  for (int a = 0; a < 3; ++a) ext = std::max(ext, root.hi[a] - root.lo[a]);
+  int e = (ext > 0) ? (int)std::ceil(std::log2(ext)) - 22 : -100;
+  e = std::max(-100, std::min(100, e));
+  while (std::ldexp(ext, -e) > double(1 << 22)) ++e;  // guard log2 rounding
+  float origin[3] = {(float)root.lo[0], (float)root.lo[1], (float)root.lo[2]};
+  // x - origin can round in fp64 when |x| << |origin| (e.g. x ~ 1e-17), so
+  // the floor/ceil estimate is corrected until origin + k 2^e (exact in fp64
+  // for these magnitudes) lies on the conservative side of x.
+  auto lat_at = [&](int64_t k, int a) { return (double)origin[a] + std::ldexp((double)k, e); };
+  auto lat_lo = [&](double x, int a) {
+    int64_t k = (int64_t)std::floor(std::ldexp(x - (double)origin[a], -e));
+    while (lat_at(k, a) > x) --k;
+    while (lat_at(k + 1, a) <= x) ++k;
+    return k;
+  };
+  auto lat_hi = [&](double x, int a) {
+    int64_t k = (int64_t)std::ceil(std::ldexp(x - (double)origin[a], -e));
+    while (lat_at(k, a) < x) ++k;
+    while (lat_at(k - 1, a) >= x) --k;
+    return k;
+  };
+
+  std::vector<int64_t> lbox(6 * (size_t)n);  // exact boxes on the lattice (conservative)
+  for (int i = 0; i < n; ++i)
+    for (int a = 0; a < 3; ++a) {
+      lbox[6 * i + a] = lat_lo(bd.nodes[i].lo[a], a);
+      lbox[6 * i + 3 + a] = lat_hi(bd.nodes[i].hi[a], a);
+    }
+  int64_t rootbox[6];
+  for (int k = 0; k < 6; ++k) rootbox[k] = lbox[k];
+
+  // ---- predictor–corrector codes, top-down against DECODED parents
+  std::vector<int64_t> dec(6 * (size_t)n);
+  std::vector<uint16_t> code(6 * (size_t)n, 0);
+  for (int k = 0; k < 6; ++k) dec[k] = rootbox[k];  // root == anchor -> zero codes
+  {
+    std::vector<int> stack = {0};
+    while (!stack.empty()) {
+      int p = stack.back(); stack.pop_back();
+      for (int ch : bd.nodes[p].children) {
+        for (int a = 0; a < 3; ++a) {
+          int64_t Plo = dec[6 * p + a], Phi = dec[6 * p + 3 + a];
+          int64_t Clo = lbox[6 * ch + a], Chi = lbox[6 * ch + 3 + a];
+          if (Clo < Plo || Chi > Phi) return set_error(CBVH_EMESH, "internal: child not inside decoded parent");
+          int s = std::max(0, bitlen64(Phi - Plo) - bits);
+          int64_t qlo = (Clo - Plo) >> s, qhi = (Phi - Chi) >> s;
+          if (qlo >= (1 << bits) || qhi >= (1 << bits)) return set_error(CBVH_EMESH, "internal: correction overflow");
+          code[6 * ch + a] = (uint16_t)qlo;
+          code[6 * ch + 3 + a] = (uint16_t)qhi;
+          dec[6 * ch + a] = Plo + (qlo << s);
+          dec[6 * ch + 3 + a] = Phi - (qhi << s);
+        }
+        stack.push_back(ch);
+      }
+    }
+  }
+
+  // ---- greedy BFS treelet packing of sibling groups (reading R6)
+  struct Group { int parent; std::vector<int> nodes; };
+  struct Treelet { int64_t anchor[6]; int first, count; };
+  std::vector<Treelet> treelets;
+  std::vector<int> new_id(n, -1), order;
+  order.reserve(n);
+  std::deque<Group> roots;
+  roots.push_back(Group{-1, {0}});
+  while (!roots.empty()) {
+    Group g0 = roots.front(); roots.pop_front();
+    Treelet tl;
+    for (int k = 0; k < 6; ++k) tl.anchor[k] = (g0.parent < 0) ? rootbox[k] : dec[6 * g0.parent + k];
+    tl.first = (int)order.size();
+    int count = 0;
+    std::deque<Group> bfs;
+    bfs.push_back(g0);
+    while (!bfs.empty()) {
+      Group g = bfs.front(); bfs.pop_front();
+      if (count + (int)g.nodes.size() > T) { roots.push_back(g); continue; }
+      for (int x : g.nodes) { new_id[x] = (int)order.size(); order.push_back(x); }
+      count += (int)g.nodes.size();
+      for (int x : g.nodes)
+        if (!bd.nodes[x].children.empty()) bfs.push_back(Group{x, bd.nodes[x].children});
+    }
+    tl.count = count;
+    treelets.push_back(tl);
+  }
+
+  // ---- triangle soup in leaf order of the new numbering
+  std::vector<uint32_t> topo(n), tri_index;
+  std::vector<float> soup;
+  tri_index.reserve(nt);
+  soup.reserve(9 * (size_t)nt);
+  int depth = 0, leaves = 0;
+  for (int nid = 0; nid < n; ++nid) {
+    const BNode& nd = bd.nodes[order[nid]];
+    depth = std::max(depth, nd.depth);
+    if (nd.children.empty()) {
+      ++leaves;
+      uint32_t first = (uint32_t)tri_index.size(), cnt = (uint32_t)(nd.tri_end - nd.tri_begin);
+      for (int k = nd.tri_begin; k < nd.tri_end; ++k) {
+        int t = bd.perm[k];
+        tri_index.push_back((uint32_t)t);
+        for (int v = 0; v < 3; ++v)
+          for (int a = 0; a < 3; ++a) soup.push_back(mesh->vertices[3 * (int64_t)mesh->triangles[3 * (int64_t)t + v] + a]);
+      }
+      topo[nid] = 0x80000000u | ((cnt - 1) << 29) | first;
+    } else {
+      uint32_t first = (uint32_t)new_id[nd.children[0]], cnt = (uint32_t)nd.children.size();
+      for (uint32_t k = 0; k < cnt; ++k)
+        if (new_id[nd.children[k]] != (int)(first + k)) return set_error(CBVH_EMESH, "internal: sibling group split");
+      topo[nid] = ((cnt - 1) << 28) | first;
+    }
+  }
+
+  // ---- serialize
+  const uint32_t w = bits <= 4 ? 4 : bits <= 8 ? 8 : 16;
+  const size_t code_bytes_node = 6 * w / 8;
+  size_t off_topo = 256;
+  size_t off_codes = align256(off_topo + 4 * (size_t)n);
+  size_t off_treelets = align256(off_codes + code_bytes_node * (size_t)n);
+  size_t off_tris = align256(off_treelets + 32 * treelets.size());
+  size_t off_tri_index = align256(off_tris + 36 * (size_t)nt);
+  size_t total = align256(off_tri_index + 4 * (size_t)nt);
+  try {
+    out.assign(total, 0);
+  } catch (const std::bad_alloc&) {
+    return set_error(CBVH_ENOMEM, "blob allocation failed");
+  }
+  std::memcpy(&out[0], "CBVH", 4);
+  put<uint32_t>(out, 4, 1u);
+  put<uint32_t>(out, 8, (uint32_t)branching);
+  put<uint32_t>(out, 12, (uint32_t)bits);
+  put<uint32_t>(out, 16, (uint32_t)T);
+  put<uint32_t>(out, 20, (uint32_t)c);
+  put<uint32_t>(out, 24, w);
+  put<uint32_t>(out, 28, (uint32_t)n);
+  put<uint32_t>(out, 32, (uint32_t)nt);
+  put<uint32_t>(out, 36, (uint32_t)treelets.size());
+  put<uint32_t>(out, 40, (uint32_t)depth);
+  put<uint32_t>(out, 44, (uint32_t)leaves);
+  put<int32_t>(out, 48, e);
+  for (int a = 0; a < 3; ++a) put<float>(out, 52 + 4 * a, origin[a]);
+  for (int k = 0; k < 6; ++k) put<int32_t>(out, 64 + 4 * k, (int32_t)rootbox[k]);
+  put<uint64_t>(out, 88, off_topo);
+  put<uint64_t>(out, 96, off_codes);
+  put<uint64_t>(out, 104, off_treelets);
+  put<uint64_t>(out, 112, off_tris);
+  put<uint64_t>(out, 120, off_tri_index);
+  put<uint64_t>(out, 128, total);
+  std::memcpy(&out[off_topo], topo.data(), 4 * (size_t)n);
+  for (int nid = 0; nid < n; ++nid) {
+    const uint16_t* q = &code[6 * (size_t)order[nid]];
+    uint8_t* dst = &out[off_codes + code_bytes_node * nid];
+    if (w == 16) {
+      std::memcpy(dst, q, 12);
+    } else if (w == 8) {
+      for (int f = 0; f < 6; ++f) dst[f] = (uint8_t)q[f];
+    } else {
+      uint32_t word = 0;
+      for (int f = 0; f < 6; ++f) word |= (uint32_t)(q[f] & 15u) << (4 * f);
+      dst[0] = word & 255u; dst[1] = (word >> 8) & 255u; dst[2] = (word >> 16) & 255u;
+    }
+  }
+  for (size_t k = 0; k < treelets.size(); ++k) {
+    size_t o = off_treelets + 32 * k;
+    for (int j = 0; j < 6; ++j) put<int32_t>(out, o + 4 * j, (int32_t)treelets[k].anchor[j]);
+    put<uint32_t>(out, o + 24, (uint32_t)treelets[k].first);
+    put<uint32_t>(out, o + 28, (uint32_t)treelets[k].count);
+  }
+  std::memcpy(&out[off_tris], soup.data(), 36 * (size_t)nt);
+  std::memcpy(&out[off_tri_index], tri_index.data(), 4 * (size_t)nt);
+  return CBVH_OK;
+}
+
+int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
+  if (!p || !h) return set_error(CBVH_EINVAL, "null blob or header");
+  if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0) return set_error(CBVH_EBLOB, "bad magic");
+  auto u32 = [&](size_t o) { uint32_t x; std::memcpy(&x, p + o, 4); return x; };
+  auto u64 = [&](size_t o) { uint64_t x; std::memcpy(&x, p + o, 8); return x; };
+  if (u32(4) != 1) return set_error(CBVH_EBLOB, "unsupported blob version");
+  h->branching = u32(8); h->bits = u32(12); h->treelet_nodes = u32(16); h->leaf_size = u32(20);
+  h->code_width = u32(24); h->num_nodes = u32(28); h->num_tris = u32(32); h->num_treelets = u32(36);
+  h->depth = u32(40); h->num_leaves = u32(44);
+  std::memcpy(&h->lattice_exp, p + 48, 4);
+  std::memcpy(h->origin, p + 52, 12);
+  std::memcpy(h->root_box, p + 64, 24);
+  h->off_topo = u64(88); h->off_codes = u64(96); h->off_treelets = u64(104);
+  h->off_tris = u64(112); h->off_tri_index = u64(120); h->total_bytes = u64(128);
+  if (h->total_bytes != bytes) return set_error(CBVH_EBLOB, "blob size does not match header");
+  if (h->branching != 2 && h->branching != 4 && h->branching != 8) return set_error(CBVH_EBLOB, "bad branching");
+  if (h->bits < 2 || h->bits > 16) return set_error(CBVH_EBLOB, "bad bits");
+  if (h->code_width != (h->bits <= 4 ? 4u : h->bits <= 8 ? 8u : 16u)) return set_error(CBVH_EBLOB, "bad code width");
+  if (h->num_nodes == 0 || h->num_tris == 0 || h->num_nodes >= (1u << 28) || h->num_tris >= (1u << 29))
+    return set_error(CBVH_EBLOB, "bad counts");
+  const uint64_t cb = 6ull * h->code_width / 8;
+  if (h->off_topo < 256 || h->off_topo + 4ull * h->num_nodes > h->off_codes ||
+      h->off_codes + cb * h->num_nodes > h->off_treelets ||
+      h->off_treelets + 32ull * h->num_treelets > h->off_tris ||
+      h->off_tris + 36ull * h->num_tris > h->off_tri_index ||
+      h->off_tri_index + 4ull * h->num_tris > h->total_bytes)
+    return set_error(CBVH_EBLOB, "bad section offsets");
+  if ((h->off_topo | h->off_codes | h->off_tris) & 15) return set_error(CBVH_EBLOB, "misaligned sections");
+  return CBVH_OK;
+}
+
+}  // namespace cbvh
+
+extern "C" {
+
+int build_compressed_bvh(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_opts* opts,
+                         uint8_t** blob, size_t* blob_bytes) {
+  if (!blob || !blob_bytes) return cbvh::set_error(CBVH_EINVAL, "null output pointer");
+  *blob = nullptr; *blob_bytes = 0;
+  std::vector<uint8_t> out;
+  int rc;
+  try {
+    rc = cbvh::build_blob(mesh, branching, bits, opts, out);
+  } catch (const std::bad_alloc&) {
+    return cbvh::set_error(CBVH_ENOMEM, "allocation failed during build");
+  } catch (...) {
+    return cbvh::set_error(CBVH_EMESH, "unexpected failure during build");
+  }
+  if (rc != CBVH_OK) return rc;
+  uint8_t* p = (uint8_t*)std::malloc(out.size());
+  if (!p) return cbvh::set_error(CBVH_ENOMEM, "blob allocation failed");
+  std::memcpy(p, out.data(), out.size());
+  *blob = p;
+  *blob_bytes = out.size();
+  return CBVH_OK;
+}
+
+void cbvh_free_blob(uint8_t* blob) { std::free(blob); }
+
+int cbvh_blob_info(const uint8_t* h_blob, size_t bytes, cbvh_info* out) {
+  if (!h_blob || !out) return cbvh::set_error(CBVH_EINVAL, "null argument");
+  int rc = cbvh::parse_header(h_blob, bytes, &out->h);
+  if (rc) return rc;
+  const cbvh_header& h = out->h;
+  out->bvh_bytes = 4ull * h.num_nodes + (6ull * h.code_width / 8) * h.num_nodes + 32ull * h.num_treelets;
+  out->tri_bytes = 36ull * h.num_tris;
+  out->bytes_per_node = (double)out->bvh_bytes / (double)h.num_nodes;
+  out->code_bytes_per_node = 6.0 * h.code_width / 8.0;
+  return CBVH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+"""Host builder + blob format (CPU; libcbvh.so loads without a GPU).
+
+Checked by the oracle's INDEPENDENT decoder (oracle/oracle.cpp re-declares the
+layout from DESIGN.md §3): containment of every decoded box, child ⊆
+parent, leaves partition the triangles, treelets partition the
+nodes and are connected, treelet size <= T; determinism; the
+SPEC arithmetic example; fault injection; compression
+invariance of the colliding pair sets and cost monotonicity.
+"""
+import ctypes as C
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2012_05348_b200 as M
+from paper_2012_05348_b200 import _lib as L
+from workloads import generators as G
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    return G.make_config(1, num_poses=256)
+
+
+@pytest.fixture(scope="module")
+def mesh16k():
+    return G.make_config(3, num_poses=1).A
+
+
+def test_library_exports_every_header_symbol():
+    text = open(L.HERE + "/../include/cbvh.h").read()
+    names = set(re.findall(r"^\s*(?:int|void|size_t|const char\*)\s+(\w+)\(", text, re.M))
+    assert {"build_compressed_bvh", "collide_batch", "distance_batch"} <= names
+    lib = L.load()
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(L.EXPORTS) == names
+
+
+@pytest.mark.parametrize("B", [2, 4, 8])
+@pytest.mark.parametrize("bits", [2, 4, 5, 8, 11, 16])
+def test_invariants_config1(cfg1, B, bits):
+    A = cfg1.A
+    bv = M.build_compressed_bvh(A.vertices, A.triangles, B, bits, 32, 4)
+    r = O.check_blob(bv.blob, A.vertices, A.triangles)
+    assert r["violations"] == 0, r
+    assert r["nodes_checked"] == bv.info["num_nodes"]
+    assert bv.info["code_width"] == (4 if bits <= 4 else 8 if bits <= 8 else 16)
+
+
+@pytest.mark.parametrize("B,bits,T", [(2, 8, 32), (4, 8, 32), (8, 16, 32), (4, 4, 64), (4, 8, 4)])
+def test_invariants_16k(mesh16k, B, bits, T):
+    bv = M.build_compressed_bvh(mesh16k.vertices, mesh16k.triangles, B, bits, T, 4)
+    r = O.check_blob(bv.blob, mesh16k.vertices, mesh16k.triangles)
+    assert r["violations"] == 0, r
+
+
+def test_node_counts_closed_form(cfg1):
+    # equal-count median split, c = 4: a binary tree over 960 triangles has
+    # 2 * 256 - 1 = 511 nodes (960 / 4 = 240 leaves -> padded split shape)
+    A = cfg1.A
+    n = {B: M.build_compressed_bvh(A.vertices, A.triangles, B, 8).info["num_nodes"] for B in (2, 4, 8)}
+    assert n == {2: 511, 4: 341, 8: 329}
+
+
+def test_determinism(cfg1):
+    A = cfg1.A
+    b1 = M.build_compressed_bvh(A.vertices, A.triangles, 4, 8).blob
+    b2 = M.build_compressed_bvh(A.vertices.copy(), A.triangles.copy(), 4, 8).blob
+    assert b1.tobytes() == b2.tobytes()
+
+
+def _tri_spanning(x0, x1):
+    return np.array([[x0, 0, 0], [x1, 0, 0], [0.5 * (x0 + x1), 1, 0]], np.float32)
+
+
+def test_spec_encode_example():
+    # parent [0, 255], child [10.7, 200], b = 8 -> q_lo = 10, q_hi = 55.
+    # On the lattice (cell 2^-14 for extent 255) the step is 2^14 cells = 1.0.
+    V = np.concatenate([_tri_spanning(10.7, 200.0), _tri_spanning(0.0, 255.0)])
+    T = np.arange(6, dtype=np.int32).reshape(2, 3)
+    bv = M.build_compressed_bvh(V, T, 2, 8, 32, 1)
+    info, blob = bv.info, bv.blob
+    assert info["num_nodes"] == 3 and info["lattice_exp"] == -14
+    topo = np.frombuffer(blob[info["off_topo"]:info["off_topo"] + 12].tobytes(), np.uint32)
+    codes = blob[info["off_codes"]:info["off_codes"] + 18].reshape(3, 6)
+    tri_index = np.frombuffer(blob[info["off_tri_index"]:info["off_tri_index"] + 8].tobytes(), np.uint32)
+    assert topo[0] >> 31 == 0 and ((topo[0] >> 28) & 7) + 1 == 2
+    assert np.all(codes[0] == 0)  # the root equals its anchor: zero corrections
+    for node in (1, 2):
+        first = topo[node] & 0x1FFFFFFF
+        if tri_index[first] == 0:  # the [10.7, 200] triangle
+            assert codes[node][0] == 10 and codes[node][3] == 55
+        else:  # the [0, 255] triangle equals the parent on x: zero corrections
+            assert codes[node][0] == 0 and codes[node][3] == 0
+    assert O.check_blob(blob, V, T)["violations"] == 0
+
+
+def test_treelet_closed_form_T_equals_B(cfg1):
+    # T = B: every sibling group opens its own treelet -> 1 + #internal treelets
+    A = cfg1.A
+    bv = M.build_compressed_bvh(A.vertices, A.triangles, 2, 8, 2, 4)
+    i = bv.info
+    assert i["num_treelets"] == 1 + (i["num_nodes"] - i["num_leaves"])
+    big = M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, 4096, 4).info
+    assert big["num_treelets"] == 1  # tree smaller than the budget
+
+
+def test_bytes_per_node_accounting(cfg1):
+    A = cfg1.A
+    for bits, cw in ((4, 3), (8, 6), (16, 12)):
+        i = M.build_compressed_bvh(A.vertices, A.triangles, 4, bits, 32).info
+        assert i["code_bytes_per_node"] == cw  # 6 corrections x field width
+        assert i["bvh_bytes"] == (4 + cw) * i["num_nodes"] + 32 * i["num_treelets"]
+        assert i["tri_bytes"] == 36 * A.num_triangles
+        assert i["code_bytes_per_node"] <= 0.25 * 24 or bits == 16  # S:344 (b=8: 6 B vs 24 B fp32)
+
+
+def test_fault_injection_detected(cfg1):
+    A = cfg1.A
+    bv = M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, 32)
+    info = bv.info
+    assert O.check_blob(bv.blob, A.vertices, A.triangles)["violations"] == 0
+    # (a) inflate one correction of a leaf: its decoded box no longer contains it
+    topo = np.frombuffer(bv.blob[info["off_topo"]:info["off_topo"] + 4 * info["num_nodes"]].tobytes(), np.uint32)
+    leaf = int(np.nonzero(topo >> 31)[0][5])
+    bad = bv.blob.copy()
+    bad[info["off_codes"] + 6 * leaf + 0] = 255
+    bad[info["off_codes"] + 6 * leaf + 3] = 255
+    r = O.check_blob(bad, A.vertices, A.triangles)
+    assert r["containment"] > 0
+    # (b) a triangle missing from the leaves
+    bad = bv.blob.copy()
+    ti = info["off_tri_index"]
+    bad[ti:ti + 4] = bad[ti + 4:ti + 8]  # triangle index 0 slot now duplicates slot 1
+    r = O.check_blob(bad, A.vertices, A.triangles)
+    assert r["triangle_partition"] > 0
+    # (c) corrupted topology word
+    bad = bv.blob.copy()
+    bad[info["off_topo"]:info["off_topo"] + 4] = np.frombuffer(np.uint32(0x0FFFFFF0).tobytes(), np.uint8)
+    r = O.check_blob(bad, A.vertices, A.triangles)
+    assert r["violations"] > 0
+
+
+@pytest.mark.parametrize("B,bits", [(2, 8), (4, 4), (4, 8), (8, 16)])
+def test_compression_invariance_and_cost(cfg1, B, bits):
+    # BJ oracle self-check (3): the pair sets from traversing the DECODED
+    # compressed boxes equal those over exact fp64 boxes; looser boxes cannot
+    # prune more.
+    A, Bm, P = cfg1.A, cfg1.B, cfg1.poses[:48]
+    ba = M.build_compressed_bvh(A.vertices, A.triangles, B, bits)
+    bb = M.build_compressed_bvh(Bm.vertices, Bm.triangles, B, bits)
+    dA = O.Tree.from_blob(ba.blob, A.vertices, A.triangles)
+    dB = O.Tree.from_blob(bb.blob, Bm.vertices, Bm.triangles)
+    eA = O.Tree.from_blob(ba.blob, A.vertices, A.triangles, exact_boxes=True)
+    eB = O.Tree.from_blob(bb.blob, Bm.vertices, Bm.triangles, exact_boxes=True)
+    rA = O.Tree.from_mesh(A.vertices, A.triangles)
+    rB = O.Tree.from_mesh(Bm.vertices, Bm.triangles)
+    hits = 0
+    for p in P:
+        s = O.collide_pairs(dA, dB, p)
+        assert s == O.collide_pairs(eA, eB, p) == O.collide_pairs(rA, rB, p)
+        hits += bool(s)
+    assert hits > 5
+    _, _, _, st_dec = O.collide(dA, dB, P, 0.0)
+    _, _, _, st_ex = O.collide(eA, eB, P, 0.0)
+    assert st_dec[0] >= st_ex[0]
+
+
+def test_error_paths():
+    lib = L.load()
+    V = np.zeros((3, 3), np.float32)
+    V[1, 0] = V[2, 1] = 1
+    T = np.array([[0, 1, 2]], np.int32)
+    ok = M.build_compressed_bvh(V, T, 2, 8)
+    assert ok.info["num_nodes"] == 1 and ok.info["num_leaves"] == 1
+    with pytest.raises(L.CbvhError, match="EINVAL"):
+        M.build_compressed_bvh(V, T, 3, 8)
+    with pytest.raises(L.CbvhError, match="EINVAL"):
+        M.build_compressed_bvh(V, T, 4, 1)
+    with pytest.raises(L.CbvhError, match="EINVAL"):
+        M.build_compressed_bvh(V, T, 4, 17)
+    with pytest.raises(L.CbvhError, match="EINVAL"):
+        M.build_compressed_bvh(V, T, 8, 8, treelet_nodes=4)
+    with pytest.raises(L.CbvhError, match="EINVAL"):
+        M.build_compressed_bvh(V, T, 4, 8, leaf_size=5)
+    with pytest.raises(L.CbvhError, match="EMESH"):
+        M.build_compressed_bvh(V, np.zeros((0, 3), np.int32), 4, 8)
+    with pytest.raises(L.CbvhError, match="EMESH"):
+        M.build_compressed_bvh(V, np.array([[0, 1, 3]], np.int32), 4, 8)
+    Vn = V.copy()
+    Vn[0, 0] = np.nan
+    with pytest.raises(L.CbvhError, match="EMESH"):
+        M.build_compressed_bvh(Vn, T, 4, 8)
+    bad = ok.blob.copy()
+    bad[0] = ord("X")
+    with pytest.raises(L.CbvhError, match="EBLOB"):
+        M.blob_info(bad)
+    with pytest.raises(L.CbvhError, match="EBLOB"):
+        M.blob_info(ok.blob[:-16])
+    info = L.cbvh_info()
+    assert lib.cbvh_blob_info(None, 0, C.byref(info)) == L.CBVH_EINVAL

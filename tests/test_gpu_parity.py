@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle.
+
+Runs only on a B200 (-m gpu).  Every input comes from workloads.generators;
+every expected value from oracle/ on the same arrays.  Sizes: config 1 in full
+(1,024 poses, several thousand warp iterations, ragged tail), tiny meshes,
+degenerate cases, and every BASELINE.json config at full size in the launch
+configuration bench.py times, compared on seeded samples of poses the oracle
+computes one by one, plus size-independent properties (hit == count > 0,
+identical counts across all 9 config-3 layouts).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from tests.parity import check_collide, check_distance
+from workloads import generators as G
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _cuda_or_fail():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test without a CUDA device")
+
+
+@pytest.fixture(scope="module")
+def M():
+    _cuda_or_fail()
+    import paper_2012_05348_b200 as M
+    return M
+
+
+def run_collide(M, A, B, poses, stats=False):
+    P = torch.from_numpy(np.ascontiguousarray(poses)).cuda()
+    ws = M.Workspace(A, B, 0)
+    hit, cnt = M.collide_batch(A, B, P, workspace=ws, stats=stats)
+    M.check(ws)
+    out = hit.cpu().numpy(), cnt.cpu().numpy().view(np.uint32).astype(np.int64)
+    if stats:
+        return out + (M.read_stats(ws),)
+    return out
+
+
+def run_distance(M, A, B, poses, stats=False):
+    P = torch.from_numpy(np.ascontiguousarray(poses)).cuda()
+    ws = M.Workspace(A, B, 1)
+    d = M.distance_batch(A, B, P, workspace=ws, stats=stats)
+    M.check(ws)
+    out = d.cpu().numpy()
+    if stats:
+        return out, M.read_stats(ws)
+    return out
+
+
+def build(M, mesh, B, bits, T=32):
+    return M.build_compressed_bvh(mesh.vertices, mesh.triangles, B, bits, T, 4).to_device()
+
+
+def oracle_trees(w):
+    return O.Tree.from_mesh(w.A.vertices, w.A.triangles), O.Tree.from_mesh(w.B.vertices, w.B.triangles)
+
+
+# ------------------------------------------------------------------ config 1 in full
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    w = G.make_config(1)
+    tA, tB = oracle_trees(w)
+    delta = O.band_delta(w.A.vertices)
+    cnt, H, Z, _ = O.collide(tA, tB, w.poses, delta)
+    return w, tA, tB, delta, cnt, H, Z
+
+
+def test_config1_full_collide(M, cfg1):
+    w, tA, tB, delta, cnt, H, Z = cfg1
+    A, B = build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet)
+    hit, gc = run_collide(M, A, B, w.poses)
+    rep = check_collide(hit, gc, H, Z, "cfg1")
+    assert rep["hits"] > 200
+    print("cfg1", rep)
+
+
+@pytest.mark.parametrize("Bf,bits", [(2, 4), (4, 8), (8, 16), (4, 2)])
+def test_config1_layouts(M, cfg1, Bf, bits):
+    w, tA, tB, delta, cnt, H, Z = cfg1
+    A, B = build(M, w.A, Bf, bits), build(M, w.B, Bf, bits)
+    hit, gc = run_collide(M, A, B, w.poses)
+    check_collide(hit, gc, H, Z, f"cfg1 B={Bf} b={bits}")
+
+
+def test_config1_stats_variant_same_answer(M, cfg1):
+    w = cfg1[0]
+    A, B = build(M, w.A, 2, 8), build(M, w.B, 2, 8)
+    h1, c1 = run_collide(M, A, B, w.poses)
+    h2, c2, st = run_collide(M, A, B, w.poses, stats=True)
+    assert np.array_equal(h1, h2) and np.array_equal(c1, c2)
+    assert st["bv_tests"] > 0 and st["tri_tests"] >= int(c1.sum())
+    assert st["expansions"] > 0 and st["leaf_pairs"] > 0
+
+
+def test_config1_distance(M, cfg1):
+    w, tA, tB, delta = cfg1[:4]
+    A, B = build(M, w.A, 2, 8), build(M, w.B, 2, 8)
+    P = w.poses[:256]
+    d64, _ = O.distance(tA, tB, P)
+    g = run_distance(M, A, B, P)
+    rep = check_distance(g, d64, delta, "cfg1 distance")
+    assert rep["near_contact"] > 20
+
+
+# ------------------------------------------------------------------ tiny + degenerate
+
+
+@pytest.mark.parametrize("which", ["8x4", "16x8"])
+def test_tiny_collide_and_distance(M, which):
+    Am, Bm, P = G.tiny_pair(which, seed=5, n_poses=3000, half_width=1.5)
+    tA, tB = O.Tree.from_mesh(Am.vertices, Am.triangles), O.Tree.from_mesh(Bm.vertices, Bm.triangles)
+    delta = O.band_delta(Am.vertices)
+    _, H, Z = O.bruteforce_collide(tA, tB, P, delta)
+    for Bf in (2, 4, 8):
+        A, B = build(M, Am, Bf, 8), build(M, Bm, Bf, 8)
+        hit, gc = run_collide(M, A, B, P)
+        check_collide(hit, gc, H, Z, f"tiny {which} B={Bf}")
+        d = run_distance(M, A, B, P[:500])
+        check_distance(d, O.bruteforce_distance(tA, tB, P[:500]), delta, f"tiny {which}")
+
+
+def test_single_triangle_meshes(M):
+    V = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], np.float32)
+    T = np.array([[0, 1, 2]], np.int32)
+    A = M.build_compressed_bvh(V, T, 2, 8).to_device()  # root is a leaf: leaf-leaf root pair
+    P = G.identity_poses(4)
+    P[1, 11] = 0.5   # lifted: no contact
+    P[2, 11] = -1e-3  # below: no contact
+    P[3, 3] = 0.2     # shifted in-plane: coplanar overlap
+    hit, gc = run_collide(M, A, A, P)
+    assert list(gc) == [1, 0, 0, 1] and list(hit) == [1, 0, 0, 1]
+    d = run_distance(M, A, A, P)
+    assert d[0] == 0 and d[3] == 0
+    assert abs(d[1] - 0.5) < 1e-6 and abs(d[2] - 1e-3) < 1e-8
+
+
+def test_self_identity_and_far(M, cfg1):
+    w = cfg1[0]
+    A = build(M, w.A, 4, 8)
+    P = G.identity_poses(3)
+    P[1, 3] = 10.0
+    P[2, 7] = -3.0
+    hit, gc = run_collide(M, A, A, P)
+    pairs = O.collide_pairs(O.Tree.from_mesh(w.A.vertices, w.A.triangles),
+                            O.Tree.from_mesh(w.A.vertices, w.A.triangles), P[0])
+    # coincident geometry: every pair is a band pair (pen = 0), count must
+    # cover at least the triangles meeting themselves and at most all touching pairs
+    assert w.A.num_triangles <= gc[0] <= len(pairs)
+    assert gc[1] == 0 and gc[2] == 0 and hit[0] == 1
+
+
+def test_empty_and_ragged_batches(M, cfg1):
+    w, tA, tB, delta, cnt, H, Z = cfg1
+    A, B = build(M, w.A, 2, 8), build(M, w.B, 2, 8)
+    hit, gc = run_collide(M, A, B, w.poses[:0])
+    assert len(hit) == 0 and len(gc) == 0
+    for n in (1, 7, 33, 257, 1023):
+        hit, gc = run_collide(M, A, B, w.poses[:n])
+        check_collide(hit, gc, H[:n], Z[:n], f"ragged {n}")
+
+
+def test_error_paths_device(M, cfg1):
+    from paper_2012_05348_b200 import _lib as L
+    w = cfg1[0]
+    A, B = build(M, w.A, 2, 8), build(M, w.B, 2, 8)
+    P = torch.from_numpy(w.poses[:64]).cuda()
+    ws = M.Workspace(A, B, 0)
+    small = M.Workspace(A, B, 0)
+    small.nbytes = 1024
+    with pytest.raises(L.CbvhError, match="EWORKSPACE"):
+        M.collide_batch(A, B, P, workspace=small)
+    Pbig = torch.zeros(65 * 12 + 1, dtype=torch.float32, device="cuda")
+    Pmis = Pbig[1:].view(65, 12)
+    with pytest.raises(L.CbvhError, match="EINVAL"):
+        M.collide_batch(A, B, Pmis, workspace=ws)
+    M.collide_batch(A, B, P, workspace=ws)
+    M.check(ws)
+    assert M.last_launch_count() == 2
+
+
+# ------------------------------------------------------------------ full-size configs, sampled
+
+
+def _sample(n_total, k, seed):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(n_total, size=k, replace=False))
+
+
+def test_config2_full_size_sampled(M):
+    w = G.make_config(2)
+    A, B = build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet)
+    hit, gc = run_collide(M, A, B, w.poses)
+    assert 0.10 < hit.mean() < 0.25
+    idx = _sample(len(w.poses), 1500, 2)
+    # bias the sample towards colliding poses so the count check has teeth
+    idx = np.unique(np.concatenate([idx, np.nonzero(hit)[0][:500]]))
+    tA, tB = oracle_trees(w)
+    delta = O.band_delta(w.A.vertices)
+    _, H, Z, _ = O.collide(tA, tB, w.poses[idx], delta)
+    rep = check_collide(hit[idx], gc[idx], H, Z, "cfg2")
+    print("cfg2", rep)
+
+
+def test_config3_all_layouts_agree(M):
+    w = G.make_config(3)
+    idx = _sample(len(w.poses), 160, 3)
+    tA, tB = oracle_trees(w)
+    delta = O.band_delta(w.A.vertices)
+    _, H, Z, _ = O.collide(tA, tB, w.poses[idx], delta)
+    ref = None
+    for Bf, bits in w.settings:
+        A, B = build(M, w.A, Bf, bits), build(M, w.B, Bf, bits)
+        hit, gc = run_collide(M, A, B, w.poses)
+        check_collide(hit[idx], gc[idx], H, Z, f"cfg3 B={Bf} b={bits}")
+        if ref is None:
+            ref = gc
+        # leaf tests are tree-independent and culling is conservative: every
+        # layout must produce the same counts on all 262,144 poses
+        assert np.array_equal(gc, ref), f"cfg3 B={Bf} b={bits} differs from B=2 b=4"
+
+
+def test_config4_distance_full_size_sampled(M):
+    w = G.make_config(4)
+    A, B = build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet)
+    d = run_distance(M, A, B, w.poses)
+    assert np.all(np.isfinite(d)) and d.min() >= 2.42 - 1e-4
+    idx = _sample(len(w.poses), 192, 4)
+    tA, tB = oracle_trees(w)
+    d64, _ = O.distance(tA, tB, w.poses[idx])
+    rep = check_distance(d[idx], d64, O.band_delta(w.A.vertices), "cfg4")
+    print("cfg4", rep)
+
+
+def test_config5_full_size_sampled(M):
+    w = G.make_config(5)
+    A, B = build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet)
+    hit, gc = run_collide(M, A, B, w.poses)
+    assert 0.02 < hit.mean() < 0.09
+    idx = _sample(len(w.poses), 600, 5)
+    idx = np.unique(np.concatenate([idx, np.nonzero(hit)[0][::500]]))
+    tA, tB = oracle_trees(w)
+    delta = O.band_delta(w.A.vertices)
+    _, H, Z, _ = O.collide(tA, tB, w.poses[idx], delta)
+    rep = check_collide(hit[idx], gc[idx], H, Z, "cfg5")
+    print("cfg5", rep)
