@@ -42,6 +42,7 @@
 
 #include "../../include/cbvh.h"
 #include "cbvh_internal.h"
+#include "leaf_geometry.cuh"
 
 namespace cbvh {
 
@@ -198,9 +199,8 @@ __device__ __forceinline__ float sat_gap(const PoseF& P, const float alo[3], con
 
 // ---------------------------------------------------------------- leaf tests
 
-struct Tri {
-  float v[3][3];
-};
+using Tri = TriT<float>;
+using Tri64 = TriT<double>;
 
 __device__ __forceinline__ Tri load_tri(const float* tris, uint32_t i) {
   const float* p = tris + 9ull * i;
@@ -210,7 +210,9 @@ __device__ __forceinline__ Tri load_tri(const float* tris, uint32_t i) {
   return T;
 }
 
-// B's world triangle into A's local frame: u = R^T (v - t).
+// B's world triangle into A's local frame: u = R^T (v - t).  Near contact
+// |v - t| is small, so the subtraction is (almost) exact and the local-frame
+// error stays ~1e-7 even at |t| = 50 (SURVEY §8(c) reading R12).
 __device__ __forceinline__ Tri to_local(const PoseF& P, const Tri& W) {
   Tri L;
   #pragma unroll
@@ -222,172 +224,24 @@ __device__ __forceinline__ Tri to_local(const PoseF& P, const Tri& W) {
   return L;
 }
 
-__device__ __forceinline__ void vsub(const float* a, const float* b, float* r) {
-  r[0] = a[0] - b[0]; r[1] = a[1] - b[1]; r[2] = a[2] - b[2];
-}
-__device__ __forceinline__ float vdot(const float* a, const float* b) {
-  return fmaf(a[0], b[0], fmaf(a[1], b[1], a[2] * b[2]));
-}
-__device__ __forceinline__ void vcross(const float* a, const float* b, float* r) {
-  r[0] = a[1] * b[2] - a[2] * b[1];
-  r[1] = a[2] * b[0] - a[0] * b[2];
-  r[2] = a[0] * b[1] - a[1] * b[0];
-}
-
-__device__ __forceinline__ float orient2(float ax, float ay, float bx, float by, float cx, float cy) {
-  return (bx - ax) * (cy - ay) - (by - ay) * (cx - ax);
-}
-
-__device__ bool seg2_intersect(const float* p1, const float* p2, const float* q1, const float* q2) {
-  float d1 = orient2(q1[0], q1[1], q2[0], q2[1], p1[0], p1[1]);
-  float d2 = orient2(q1[0], q1[1], q2[0], q2[1], p2[0], p2[1]);
-  float d3 = orient2(p1[0], p1[1], p2[0], p2[1], q1[0], q1[1]);
-  float d4 = orient2(p1[0], p1[1], p2[0], p2[1], q2[0], q2[1]);
-  if (((d1 > 0.f && d2 < 0.f) || (d1 < 0.f && d2 > 0.f)) && ((d3 > 0.f && d4 < 0.f) || (d3 < 0.f && d4 > 0.f)))
-    return true;
-  auto on = [](const float* a, const float* b, const float* c) {
-    return fminf(a[0], b[0]) <= c[0] && c[0] <= fmaxf(a[0], b[0]) && fminf(a[1], b[1]) <= c[1] &&
-           c[1] <= fmaxf(a[1], b[1]);
-  };
-  return (d1 == 0.f && on(q1, q2, p1)) || (d2 == 0.f && on(q1, q2, p2)) || (d3 == 0.f && on(p1, p2, q1)) ||
-         (d4 == 0.f && on(p1, p2, q2));
-}
-
-__device__ bool pt_in_tri2(const float* p, const float* a, const float* b, const float* c) {
-  float o1 = orient2(a[0], a[1], b[0], b[1], p[0], p[1]);
-  float o2 = orient2(b[0], b[1], c[0], c[1], p[0], p[1]);
-  float o3 = orient2(c[0], c[1], a[0], a[1], p[0], p[1]);
-  bool neg = (o1 < 0.f) || (o2 < 0.f) || (o3 < 0.f);
-  bool pos = (o1 > 0.f) || (o2 > 0.f) || (o3 > 0.f);
-  return !(neg && pos);
-}
-
-__device__ __noinline__ bool coplanar2(const float* N, const Tri& V, const Tri& U) {
-  float a0 = fabsf(N[0]), a1 = fabsf(N[1]), a2 = fabsf(N[2]);
-  int i0, i1;
-  if (a0 >= a1 && a0 >= a2) { i0 = 1; i1 = 2; }
-  else if (a1 >= a2) { i0 = 0; i1 = 2; }
-  else { i0 = 0; i1 = 1; }
-  float v[3][2], u[3][2];
-  for (int k = 0; k < 3; ++k) {
-    v[k][0] = V.v[k][i0]; v[k][1] = V.v[k][i1];
-    u[k][0] = U.v[k][i0]; u[k][1] = U.v[k][i1];
+// fp64 re-evaluation of a near-contact distance candidate:
+// the same inputs (fp32 A triangle, fp32 world B triangle, fp32 pose) lifted
+// exactly to fp64, so the result meets the 1e-5 relative tolerance at any d.
+__device__ __noinline__ float tri_dist_fp64(const PoseF& P, const float* trisA, uint32_t ia,
+                                            const float* trisB, uint32_t ib) {
+  Tri64 a, b;
+  #pragma unroll
+  for (int k = 0; k < 9; ++k) a.v[k / 3][k % 3] = (double)__ldg(trisA + 9ull * ia + k);
+  #pragma unroll
+  for (int v = 0; v < 3; ++v) {
+    double d0 = (double)__ldg(trisB + 9ull * ib + 3 * v) - (double)P.t[0];
+    double d1 = (double)__ldg(trisB + 9ull * ib + 3 * v + 1) - (double)P.t[1];
+    double d2 = (double)__ldg(trisB + 9ull * ib + 3 * v + 2) - (double)P.t[2];
+    #pragma unroll
+    for (int k = 0; k < 3; ++k)
+      b.v[v][k] = fma((double)P.R[0][k], d0, fma((double)P.R[1][k], d1, (double)P.R[2][k] * d2));
   }
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j)
-      if (seg2_intersect(v[i], v[(i + 1) % 3], u[j], u[(j + 1) % 3])) return true;
-  return pt_in_tri2(v[0], u[0], u[1], u[2]) || pt_in_tri2(u[0], v[0], v[1], v[2]);
-}
-
-// interval of a triangle on the line of the two planes (Möller 1997):
-// the vertex alone on its side k, crossing points toward i and j.
-__device__ __forceinline__ bool interval(const float p[3], const float d[3], float* t0, float* t1) {
-  int k, i, j;
-  if (d[0] * d[1] > 0.f) { k = 2; i = 0; j = 1; }
-  else if (d[0] * d[2] > 0.f) { k = 1; i = 0; j = 2; }
-  else if (d[1] * d[2] > 0.f || d[0] != 0.f) { k = 0; i = 1; j = 2; }
-  else if (d[1] != 0.f) { k = 1; i = 0; j = 2; }
-  else if (d[2] != 0.f) { k = 2; i = 0; j = 1; }
-  else return false;
-  float a = p[k] + (p[i] - p[k]) * __fdividef(d[k], d[k] - d[i]);
-  float b = p[k] + (p[j] - p[k]) * __fdividef(d[k], d[k] - d[j]);
-  *t0 = fminf(a, b);
-  *t1 = fmaxf(a, b);
-  return true;
-}
-
-__device__ bool tri_tri_overlap(const Tri& V, const Tri& U) {
-  float e1[3], e2[3], N1[3], N2[3];
-  vsub(V.v[1], V.v[0], e1); vsub(V.v[2], V.v[0], e2); vcross(e1, e2, N1);
-  float d1 = -vdot(N1, V.v[0]);
-  float du[3] = {vdot(N1, U.v[0]) + d1, vdot(N1, U.v[1]) + d1, vdot(N1, U.v[2]) + d1};
-  if ((du[0] > 0.f && du[1] > 0.f && du[2] > 0.f) || (du[0] < 0.f && du[1] < 0.f && du[2] < 0.f)) return false;
-  vsub(U.v[1], U.v[0], e1); vsub(U.v[2], U.v[0], e2); vcross(e1, e2, N2);
-  float d2 = -vdot(N2, U.v[0]);
-  float dv[3] = {vdot(N2, V.v[0]) + d2, vdot(N2, V.v[1]) + d2, vdot(N2, V.v[2]) + d2};
-  if ((dv[0] > 0.f && dv[1] > 0.f && dv[2] > 0.f) || (dv[0] < 0.f && dv[1] < 0.f && dv[2] < 0.f)) return false;
-  if (du[0] == 0.f && du[1] == 0.f && du[2] == 0.f) return coplanar2(N1, V, U);
-  float D[3];
-  vcross(N1, N2, D);
-  int ax = 0;
-  float m = fabsf(D[0]);
-  if (fabsf(D[1]) > m) { m = fabsf(D[1]); ax = 1; }
-  if (fabsf(D[2]) > m) { m = fabsf(D[2]); ax = 2; }
-  if (m == 0.f) return coplanar2(N1, V, U);
-  float vp[3] = {V.v[0][ax], V.v[1][ax], V.v[2][ax]};
-  float up[3] = {U.v[0][ax], U.v[1][ax], U.v[2][ax]};
-  float a0, a1, b0, b1;
-  if (!interval(vp, dv, &a0, &a1) || !interval(up, du, &b0, &b1)) return coplanar2(N1, V, U);
-  return !(a1 < b0 || b1 < a0);
-}
-
-__device__ __forceinline__ float pt_seg_d2(const float* p, const float* a, const float* b) {
-  float ab[3], ap[3];
-  vsub(b, a, ab); vsub(p, a, ap);
-  float L = vdot(ab, ab);
-  float t = L > 0.f ? __saturatef(vdot(ap, ab) / L) : 0.f;
-  float q[3] = {fmaf(t, ab[0], a[0]) - p[0], fmaf(t, ab[1], a[1]) - p[1], fmaf(t, ab[2], a[2]) - p[2]};
-  return vdot(q, q);
-}
-
-// min over (s,t) in [0,1]^2: the stationary point when inside, else the four
-// boundary point–segment distances; any candidate is a real pair of points,
-// so rounding can only over-estimate the minimum.
-__device__ float seg_seg_d2(const float* p0, const float* p1, const float* q0, const float* q1) {
-  float best = fminf(fminf(pt_seg_d2(p0, q0, q1), pt_seg_d2(p1, q0, q1)),
-                     fminf(pt_seg_d2(q0, p0, p1), pt_seg_d2(q1, p0, p1)));
-  float d1[3], d2[3], r[3];
-  vsub(p1, p0, d1); vsub(q1, q0, d2); vsub(p0, q0, r);
-  float a = vdot(d1, d1), e = vdot(d2, d2), b = vdot(d1, d2), c = vdot(d1, r), f = vdot(d2, r);
-  float den = a * e - b * b;
-  if (den > 0.f) {
-    float s = (b * f - c * e) / den, t = (a * f - b * c) / den;
-    if (s >= 0.f && s <= 1.f && t >= 0.f && t <= 1.f) {
-      float w[3] = {r[0] + s * d1[0] - t * d2[0], r[1] + s * d1[1] - t * d2[1], r[2] + s * d1[2] - t * d2[2]};
-      best = fminf(best, vdot(w, w));
-    }
-  }
-  return best;
-}
-
-__device__ float pt_tri_d2(const float* p, const Tri& T) {
-  float e1[3], e2[3], n[3], w[3];
-  vsub(T.v[1], T.v[0], e1); vsub(T.v[2], T.v[0], e2); vcross(e1, e2, n);
-  float best = fminf(fminf(pt_seg_d2(p, T.v[0], T.v[1]), pt_seg_d2(p, T.v[1], T.v[2])), pt_seg_d2(p, T.v[2], T.v[0]));
-  float nn = vdot(n, n);
-  if (nn > 0.f) {
-    vsub(p, T.v[0], w);
-    float h = vdot(w, n) / nn;
-    float q[3] = {p[0] - h * n[0], p[1] - h * n[1], p[2] - h * n[2]};
-    float a[3], b[3], c0[3];
-    vsub(T.v[1], T.v[0], a); vsub(q, T.v[0], b); vcross(a, b, c0);
-    bool in = vdot(c0, n) >= 0.f;
-    vsub(T.v[2], T.v[1], a); vsub(q, T.v[1], b); vcross(a, b, c0);
-    in = in && vdot(c0, n) >= 0.f;
-    vsub(T.v[0], T.v[2], a); vsub(q, T.v[2], b); vcross(a, b, c0);
-    in = in && vdot(c0, n) >= 0.f;
-    if (in) {
-      float d = p[0] - q[0], e = p[1] - q[1], f = p[2] - q[2];
-      best = fminf(best, d * d + e * e + f * f);
-    }
-  }
-  return best;
-}
-
-__device__ float tri_tri_dist(const Tri& V, const Tri& U) {
-  if (tri_tri_overlap(V, U)) return 0.f;
-  float best = FLT_MAX;
-  #pragma unroll 1
-  for (int k = 0; k < 3; ++k) {
-    best = fminf(best, pt_tri_d2(V.v[k], U));
-    best = fminf(best, pt_tri_d2(U.v[k], V));
-  }
-  #pragma unroll 1
-  for (int i = 0; i < 3; ++i)
-    #pragma unroll 1
-    for (int j = 0; j < 3; ++j)
-      best = fminf(best, seg_seg_d2(V.v[i], V.v[(i + 1) % 3], U.v[j], U.v[(j + 1) % 3]));
-  return sqrtf(best);
+  return (float)tri_tri_dist(a, b);
 }
 
 // ----------------------------------------------------------------------------
@@ -406,245 +260,253 @@ __device__ __forceinline__ int tri_pair_count(uint32_t ta, uint32_t tb) {
   return (int)(((ta >> 29) & 3u) + 1) * (int)(((tb >> 29) & 3u) + 1);
 }
 
-template <int MODE, bool STATS>
-struct Warp {
-  uint32_t* st;      // stack SoA [kFields][kStack]
-  uint32_t* lq;      // leaf queue SoA [3][kLeafQ]: pose, topoA, topoB
-  uint32_t* spill;   // this warp's global spill area
+// per-warp constant context (registers); mutable counters live in the kernel
+struct WarpCtx {
+  uint32_t* st;     // stack SoA [kFields][kStack]
+  uint32_t* lq;     // leaf queue SoA [3][kLeafQ]: pose, topoA, topoB
+  uint32_t* spill;  // this warp's global spill area [kSpillCap][kFields]
   int lane;
-  int top, nleaf, spill_top;
-  unsigned long long s_bv, s_exp, s_leaf, s_tri, s_dec, s_spill;
 };
 
-template <int MODE, bool STATS>
-__device__ __noinline__ void drain_leaves(const Params& p, Warp<MODE, STATS>& w) {
-  // process every queued leaf pair: tri pairs spread over the 32 lanes
+// Drain the leaf queue: checkPrimitives over every queued leaf pair,
+// the c_A x c_B triangle pairs spread over the 32 lanes.  Returns the number
+// of triangle-pair tests (for stats).
+template <int MODE>
+__device__ __noinline__ unsigned drain_leaves(const Params& p, const WarpCtx c, int nleaf) {
+  unsigned tests = 0;
   int head = 0;
-  while (head < w.nleaf) {
-    int avail = min(32, w.nleaf - head);
+  while (head < nleaf) {
+    int avail = min(32, nleaf - head);
     uint32_t pose = 0, ta = 0, tb = 0;
     int n = 0;
-    if (w.lane < avail) {
-      pose = w.lq[0 * kLeafQ + head + w.lane];
-      ta = w.lq[1 * kLeafQ + head + w.lane];
-      tb = w.lq[2 * kLeafQ + head + w.lane];
+    if (c.lane < avail) {
+      pose = c.lq[0 * kLeafQ + head + c.lane];
+      ta = c.lq[1 * kLeafQ + head + c.lane];
+      tb = c.lq[2 * kLeafQ + head + c.lane];
       n = tri_pair_count(ta, tb);
     }
     int incl = n;
     #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int y = __shfl_up_sync(FULL, incl, o);
-      if (w.lane >= o) incl += y;
+      if (c.lane >= o) incl += y;
     }
-    unsigned fit = __ballot_sync(FULL, w.lane < avail && incl <= 32);
-    int m = __popc(fit);  // >= 1 since every entry has <= 16 tri pairs
-    int total = __shfl_sync(FULL, incl, m - 1);
-    unsigned starts = __reduce_or_sync(FULL, (w.lane < m) ? (1u << (incl - n)) : 0u);
-    // this lane's tri pair
-    int e = __popc(starts & ((2u << w.lane) - 1u)) - 1;
-    int start_e = __shfl_sync(FULL, incl - n, e < 0 ? 0 : e);
-    uint32_t my_pose = __shfl_sync(FULL, pose, e < 0 ? 0 : e);
-    uint32_t my_ta = __shfl_sync(FULL, ta, e < 0 ? 0 : e);
-    uint32_t my_tb = __shfl_sync(FULL, tb, e < 0 ? 0 : e);
-    bool valid = w.lane < total;
-    int k = w.lane - start_e;
-    int nb = (int)((my_tb >> 29) & 3u) + 1;
-    uint32_t ia = (my_ta & 0x1FFFFFFFu) + (uint32_t)(k / nb);
-    uint32_t ib = (my_tb & 0x1FFFFFFFu) + (uint32_t)(k % nb);
+    const unsigned fit = __ballot_sync(FULL, c.lane < avail && incl <= 32);
+    const int m = __popc(fit);  // >= 2: an entry has at most 16 triangle pairs
+    const int total = __shfl_sync(FULL, incl, m - 1);
+    const unsigned starts = __reduce_or_sync(FULL, (c.lane < m) ? (1u << (incl - n)) : 0u);
+    int e = __popc(starts & ((2u << c.lane) - 1u)) - 1;
+    const int start_e = __shfl_sync(FULL, incl - n, e);
+    const uint32_t my_pose = __shfl_sync(FULL, pose, e);
+    const uint32_t my_ta = __shfl_sync(FULL, ta, e);
+    const uint32_t my_tb = __shfl_sync(FULL, tb, e);
+    const bool valid = c.lane < total;
+    const int k = c.lane - start_e;
+    const int nb = (int)((my_tb >> 29) & 3u) + 1;
+    const uint32_t ia = (my_ta & 0x1FFFFFFFu) + (uint32_t)(k / nb);
+    const uint32_t ib = (my_tb & 0x1FFFFFFFu) + (uint32_t)(k % nb);
     bool hit = false;
     float d = FLT_MAX;
     if (valid) {
-      PoseF P = load_pose(p.poses, (int)my_pose);
-      Tri TA = load_tri(p.A.tris, ia);
-      Tri TB = to_local(P, load_tri(p.B.tris, ib));
-      if (MODE == 0) hit = tri_tri_overlap(TA, TB);
-      else d = tri_tri_dist(TA, TB);
+      const PoseF P = load_pose(p.poses, (int)my_pose);
+      const Tri TA = load_tri(p.A.tris, ia);
+      const Tri TB = to_local(P, load_tri(p.B.tris, ib));
+      if (MODE == 0) {
+        hit = tri_tri_overlap(TA, TB);
+      } else {
+        d = tri_tri_dist(TA, TB);
+        // fp32 error here is ~1e-7 x (|t| + model extents); candidates whose
+        // distance is too small for a 1e-5 relative bound are re-evaluated in
+        // fp64
+        const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
+        if (d < 0.05f * (tmax + p.A.maxabs + p.B.maxabs)) d = tri_dist_fp64(P, p.A.tris, ia, p.B.tris, ib);
+      }
     }
-    if (STATS) {
-      if (w.lane == 0) { w.s_tri += total; w.s_leaf += m; }
-    }
+    tests += (unsigned)total;
     if (MODE == 0) {
-      unsigned hm = __ballot_sync(FULL, hit);
+      const unsigned hm = __ballot_sync(FULL, hit);
       if (hit) {
-        unsigned g = __match_any_sync(hm, my_pose);
-        if (w.lane == __ffs(g) - 1) {
+        const unsigned g = __match_any_sync(hm, my_pose);
+        if (c.lane == __ffs(g) - 1) {
           atomicAdd(&p.count[my_pose], (unsigned)__popc(g));
           p.hit[my_pose] = 1;
         }
       }
     } else {
-      unsigned vm = __ballot_sync(FULL, valid);
+      const unsigned vm = __ballot_sync(FULL, valid);
       if (valid) {
-        unsigned g = __match_any_sync(vm, my_pose);
-        unsigned mn = __reduce_min_sync(g, __float_as_uint(d));
-        if (w.lane == __ffs(g) - 1) atomicMin(&p.dist_bits[my_pose], mn);
+        const unsigned g = __match_any_sync(vm, my_pose);
+        const unsigned mn = __reduce_min_sync(g, __float_as_uint(d));
+        if (c.lane == __ffs(g) - 1) atomicMin(&p.dist_bits[my_pose], mn);
       }
     }
     head += m;
   }
-  w.nleaf = 0;
   __syncwarp();
+  return tests;
 }
 
-template <int MODE, bool STATS>
-__device__ __noinline__ void spill_out(const Params& p, Warp<MODE, STATS>& w) {
-  // move the bottom half of the smem stack to the global spill area
+// Move the bottom half of the smem stack to the warp's global spill area.
+// Returns the new (top, spill_top); on overflow flags CBVH_EOVERFLOW.
+__device__ __noinline__ int2 spill_out(const Params& p, const WarpCtx c, int top, int spill_top) {
   constexpr int H = kStack / 2;
-  if (w.spill_top + H > kSpillCap) {
-    if (w.lane == 0) atomicExch(&p.ctl->error, (unsigned)(-CBVH_EOVERFLOW));
-    w.top = 0;  // abandon: results are flagged invalid via cbvh_check
-    return;
+  if (spill_top + H > kSpillCap) {
+    if (c.lane == 0) atomicExch(&p.ctl->error, (unsigned)(-CBVH_EOVERFLOW));
+    return make_int2(0, spill_top);  // abandon; cbvh_check reports the error
   }
   __syncwarp();
-  for (int idx = w.lane; idx < H * kFields; idx += 32) {
+  for (int idx = c.lane; idx < H * kFields; idx += 32) {
     int e = idx / kFields, f = idx % kFields;
-    w.spill[(size_t)(w.spill_top + e) * kFields + f] = w.st[f * kStack + e];
+    c.spill[(size_t)(spill_top + e) * kFields + f] = c.st[f * kStack + e];
   }
   __syncwarp();
-  int rest = w.top - H;
-  for (int idx = w.lane; idx < rest * kFields; idx += 32) {
+  const int rest = top - H;
+  for (int idx = c.lane; idx < rest * kFields; idx += 32) {
     int e = idx % rest, f = idx / rest;
-    w.st[f * kStack + e] = w.st[f * kStack + e + H];
+    c.st[f * kStack + e] = c.st[f * kStack + e + H];
   }
   __syncwarp();
-  w.spill_top += H;
-  w.top = rest;
-  if (STATS && w.lane == 0) w.s_spill++;
+  return make_int2(rest, spill_top + H);
 }
 
-template <int MODE, bool STATS>
-__device__ __noinline__ void spill_in(const Params& p, Warp<MODE, STATS>& w) {
-  int n = min(kStack / 2, w.spill_top);
-  int base = w.spill_top - n;
+// Refill an empty smem stack from the top of the spill area.
+__device__ __noinline__ int2 spill_in(const WarpCtx c, int spill_top) {
+  const int n = min(kStack / 2, spill_top);
+  const int base = spill_top - n;
   __syncwarp();
-  for (int idx = w.lane; idx < n * kFields; idx += 32) {
+  for (int idx = c.lane; idx < n * kFields; idx += 32) {
     int e = idx / kFields, f = idx % kFields;
-    w.st[f * kStack + e] = w.spill[(size_t)(base + e) * kFields + f];
+    c.st[f * kStack + e] = c.spill[(size_t)(base + e) * kFields + f];
   }
   __syncwarp();
-  w.spill_top = base;
-  w.top = n;
+  return make_int2(n, base);
 }
 
 template <int MODE, bool STATS>
-__global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const Params p) {
+__global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint32_t smem[];
   const int wib = threadIdx.x >> 5;
-  Warp<MODE, STATS> w;
-  w.lane = threadIdx.x & 31;
-  w.st = smem + wib * kWarpSmemWords;
-  w.lq = w.st + kFields * kStack;
-  const int gwarp = blockIdx.x * kWarps + wib;
-  w.spill = p.spill + (size_t)gwarp * kSpillCap * kFields;
-  w.top = 0; w.nleaf = 0; w.spill_top = 0;
-  w.s_bv = w.s_exp = w.s_leaf = w.s_tri = w.s_dec = w.s_spill = 0;
+  WarpCtx c;
+  c.lane = threadIdx.x & 31;
+  c.st = smem + wib * kWarpSmemWords;
+  c.lq = c.st + kFields * kStack;
+  c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * kFields;
+  int top = 0, nleaf = 0, spill_top = 0;
+  unsigned long long s_bv = 0, s_exp = 0, s_leaf = 0, s_tri = 0, s_dec = 0, s_rec = 0, s_spill = 0;
   bool poses_left = true;
   const unsigned lt = lanemask_lt();
   const float scale_ab = p.A.maxabs + p.B.maxabs;
+  const bool root_leafpair = (p.A.root_topo & kLeafBit) && (p.B.root_topo & kLeafBit);
 
   while (true) {
-    // ---- acquire poses when the stack runs low: push the root pair
-    if (poses_left && w.top < kLowWater) {
+    // ---- acquire poses when the stack runs low: push their root pairs
+    if (poses_left && top < kLowWater) {
       unsigned base = 0;
-      if (w.lane == 0) base = atomicAdd(&p.ctl->cursor, (unsigned)kGrab);
+      if (c.lane == 0) base = atomicAdd(&p.ctl->cursor, (unsigned)kGrab);
       base = __shfl_sync(FULL, base, 0);
       if (base >= (unsigned)p.N) {
         poses_left = false;
       } else {
-        int k = min(kGrab, p.N - (int)base);
-        bool mine = w.lane < k;
-        bool leafpair = (p.A.root_topo & kLeafBit) && (p.B.root_topo & kLeafBit);
-        if (mine && !leafpair) {
-          int slot = w.top + w.lane;
-          w.st[F_POSE * kStack + slot] = base + w.lane;
-          w.st[F_TA * kStack + slot] = p.A.root_topo;
-          w.st[F_TB * kStack + slot] = p.B.root_topo;
-          #pragma unroll
-          for (int q = 0; q < 6; ++q) {
-            w.st[(F_BA + q) * kStack + slot] = (uint32_t)p.A.root[q];
-            w.st[(F_BB + q) * kStack + slot] = (uint32_t)p.B.root[q];
+        const int k = min(kGrab, p.N - (int)base);
+        if (c.lane < k) {
+          if (root_leafpair) {
+            const int slot = nleaf + c.lane;
+            c.lq[0 * kLeafQ + slot] = base + c.lane;
+            c.lq[1 * kLeafQ + slot] = p.A.root_topo;
+            c.lq[2 * kLeafQ + slot] = p.B.root_topo;
+          } else {
+            const int slot = top + c.lane;
+            c.st[F_POSE * kStack + slot] = base + c.lane;
+            c.st[F_TA * kStack + slot] = p.A.root_topo;
+            c.st[F_TB * kStack + slot] = p.B.root_topo;
+            #pragma unroll
+            for (int q = 0; q < 6; ++q) {
+              c.st[(F_BA + q) * kStack + slot] = (uint32_t)p.A.root[q];
+              c.st[(F_BB + q) * kStack + slot] = (uint32_t)p.B.root[q];
+            }
+            c.st[F_LB * kStack + slot] = 0u;
           }
-          w.st[F_LB * kStack + slot] = 0u;
         }
-        if (mine && leafpair) {
-          int slot = w.nleaf + w.lane;
-          w.lq[0 * kLeafQ + slot] = base + w.lane;
-          w.lq[1 * kLeafQ + slot] = p.A.root_topo;
-          w.lq[2 * kLeafQ + slot] = p.B.root_topo;
-        }
-        if (leafpair) w.nleaf += k; else w.top += k;
+        if (root_leafpair) nleaf += k; else top += k;
         __syncwarp();
-        if (w.nleaf > kLeafQ - 32) drain_leaves<MODE, STATS>(p, w);
+        if (nleaf > kLeafQ - 32) {
+          s_tri += drain_leaves<MODE>(p, c, nleaf);
+          nleaf = 0;
+        }
       }
     }
-    if (w.top == 0) {
-      if (w.spill_top > 0) { spill_in<MODE, STATS>(p, w); continue; }
+    if (top == 0) {
+      if (spill_top > 0) {
+        int2 r = spill_in(c, spill_top);
+        top = r.x; spill_top = r.y;
+        continue;
+      }
       if (poses_left) continue;
       break;
     }
 
     // ---- pop as many items as fill 32 lanes with child pairs
     int n = 0;
-    if (w.lane < w.top) {
-      int slot = w.top - 1 - w.lane;
-      n = pair_count(w.st[F_TA * kStack + slot], w.st[F_TB * kStack + slot]);
+    if (c.lane < top) {
+      const int slot = top - 1 - c.lane;
+      n = pair_count(c.st[F_TA * kStack + slot], c.st[F_TB * kStack + slot]);
     }
     int incl = n;
     #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int y = __shfl_up_sync(FULL, incl, o);
-      if (w.lane >= o) incl += y;
+      if (c.lane >= o) incl += y;
     }
     const int n0 = __shfl_sync(FULL, n, 0);
     int m, total, passes;
     unsigned starts;
-    if (n0 > 32) {  // B = 8 both internal: one item, two passes
+    if (n0 > 32) {  // B = 8, both internal: one item in two passes
       m = 1; total = n0; passes = (n0 + 31) >> 5; starts = 1u;
     } else {
-      unsigned fit = __ballot_sync(FULL, w.lane < w.top && incl <= 32);
+      const unsigned fit = __ballot_sync(FULL, c.lane < top && incl <= 32);
       m = __popc(fit);
       total = __shfl_sync(FULL, incl, m - 1);
       passes = 1;
-      starts = __reduce_or_sync(FULL, (w.lane < m) ? (1u << (incl - n)) : 0u);
+      starts = __reduce_or_sync(FULL, (c.lane < m) ? (1u << (incl - n)) : 0u);
     }
-    int e = __popc(starts & ((2u << w.lane) - 1u)) - 1;
-    if (e < 0) e = 0;
+    const int e = __popc(starts & ((2u << c.lane) - 1u)) - 1;
     const int start_e = __shfl_sync(FULL, incl - n, e);
-    // this lane's item, read from the stack before anything is pushed
-    const int slot = w.top - 1 - e;
-    const uint32_t pose = w.st[F_POSE * kStack + slot];
-    const uint32_t ta = w.st[F_TA * kStack + slot];
-    const uint32_t tb = w.st[F_TB * kStack + slot];
+    // this lane's item, read before anything is pushed over it
+    const int slot = top - 1 - e;
+    const uint32_t pose = c.st[F_POSE * kStack + slot];
+    const uint32_t ta = c.st[F_TA * kStack + slot];
+    const uint32_t tb = c.st[F_TB * kStack + slot];
     int32_t BA[6], BB[6];
     #pragma unroll
     for (int q = 0; q < 6; ++q) {
-      BA[q] = (int32_t)w.st[(F_BA + q) * kStack + slot];
-      BB[q] = (int32_t)w.st[(F_BB + q) * kStack + slot];
+      BA[q] = (int32_t)c.st[(F_BA + q) * kStack + slot];
+      BB[q] = (int32_t)c.st[(F_BB + q) * kStack + slot];
     }
-    const float item_lb = __uint_as_float(w.st[F_LB * kStack + slot]);
+    const float item_lb = __uint_as_float(c.st[F_LB * kStack + slot]);
     __syncwarp();
-    w.top -= m;
-    if (STATS && w.lane == 0) w.s_exp += m;
+    top -= m;
+    if (STATS) s_exp += m;
 
     const PoseF P = load_pose(p.poses, (int)pose);
-    const float eps = 2e-6f * (fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2]))) + scale_ab);
+    const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
+    const float eps = 2e-6f * (tmax + scale_ab);
     float best = FLT_MAX;
     if (MODE == 1) best = __uint_as_float(__ldcg(&p.dist_bits[pose]));
     const bool a_int = !(ta & kLeafBit), b_int = !(tb & kLeafBit);
     const int nb = b_int ? (int)((tb >> 28) & 7u) + 1 : 1;
 
     for (int pass = 0; pass < passes; ++pass) {
-      const int k = w.lane - start_e + 32 * pass;
-      bool valid = (w.lane + 32 * pass) < total;
+      const int k = c.lane - start_e + 32 * pass;
+      bool valid = (c.lane + 32 * pass) < total;
       if (MODE == 1) valid = valid && item_lb < best;
-      const int i = k / nb, j = k - (k / nb) * nb;
+      const int i = k / nb, j = k - i * nb;
       int32_t CA[6], CB[6];
       uint32_t cta = ta, ctb = tb;
       bool surv = false;
       float lb = 0.f;
       if (valid) {
         if (a_int) {
-          uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
+          const uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
           uint32_t q[6];
           load_codes(p.A, node, q);
           cta = __ldg(p.A.topo + node);
@@ -654,7 +516,7 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const Params p) {
           for (int r = 0; r < 6; ++r) CA[r] = BA[r];
         }
         if (b_int) {
-          uint32_t node = (tb & 0x0FFFFFFFu) + (uint32_t)j;
+          const uint32_t node = (tb & 0x0FFFFFFFu) + (uint32_t)j;
           uint32_t q[6];
           load_codes(p.B, node, q);
           ctb = __ldg(p.B.topo + node);
@@ -672,88 +534,83 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const Params p) {
           sat_gap<true>(P, alo, ahi, blo, bhi, eps, &lb);
           surv = lb < best;
         }
-        if (STATS) w.s_dec += (a_int ? 1 : 0) + (b_int ? 1 : 0);
+        if (STATS) {
+          s_dec += (a_int ? 1 : 0) + (b_int ? 1 : 0);
+          s_rec += (a_int ? 4 + 3 * p.A.width / 4 : 0) + (b_int ? 4 + 3 * p.B.width / 4 : 0);
+        }
       }
-      if (STATS) {
-        unsigned vm = __ballot_sync(FULL, valid);
-        if (w.lane == 0) w.s_bv += __popc(vm);
-      }
+      if (STATS) s_bv += __popc(__ballot_sync(FULL, valid)) * (c.lane == 0 ? 1 : 0);
       const bool leafpair = surv && (cta & kLeafBit) && (ctb & kLeafBit);
       const bool push = surv && !leafpair;
-      // ---- compaction: internal pairs onto the stack
+      // ---- ballot/popc compaction: internal pairs back onto the stack
       const unsigned pm = __ballot_sync(FULL, push);
       if (pm) {
-        if (w.top + 32 > kStack) spill_out<MODE, STATS>(p, w);
-        unsigned order = pm;
-        if (MODE == 1) {
-          // nearest-first: the smallest lower bound goes on top
-          unsigned key = push ? __float_as_uint(fmaxf(lb, 0.f)) : 0xffffffffu;
-          unsigned mn = __reduce_min_sync(FULL, key);
-          unsigned who = __ballot_sync(FULL, push && key == mn);
-          int wl = __ffs(who) - 1;
-          int last = 31 - __clz(pm);
-          // swap slots of lanes wl and last
-          int pos = __popc(pm & lt);
-          if (w.lane == wl) pos = __popc(pm) - 1;
-          else if (w.lane == last) pos = __popc(pm & ((1u << wl) - 1u));
-          if (push) {
-            int s2 = w.top + pos;
-            w.st[F_POSE * kStack + s2] = pose;
-            w.st[F_TA * kStack + s2] = cta;
-            w.st[F_TB * kStack + s2] = ctb;
-            #pragma unroll
-            for (int q = 0; q < 6; ++q) {
-              w.st[(F_BA + q) * kStack + s2] = (uint32_t)CA[q];
-              w.st[(F_BB + q) * kStack + s2] = (uint32_t)CB[q];
-            }
-            w.st[F_LB * kStack + s2] = __float_as_uint(lb);
-          }
-          (void)order;
-        } else {
-          if (push) {
-            int s2 = w.top + __popc(pm & lt);
-            w.st[F_POSE * kStack + s2] = pose;
-            w.st[F_TA * kStack + s2] = cta;
-            w.st[F_TB * kStack + s2] = ctb;
-            #pragma unroll
-            for (int q = 0; q < 6; ++q) {
-              w.st[(F_BA + q) * kStack + s2] = (uint32_t)CA[q];
-              w.st[(F_BB + q) * kStack + s2] = (uint32_t)CB[q];
-            }
-          }
+        if (top + 32 > kStack) {
+          int2 r = spill_out(p, c, top, spill_top);
+          top = r.x; spill_top = r.y;
+          if (STATS) s_spill++;
         }
-        w.top += __popc(pm);
+        int pos = __popc(pm & lt);
+        if (MODE == 1) {
+          // nearest-first: the smallest lower bound goes on top of the stack
+          const unsigned key = push ? __float_as_uint(fmaxf(lb, 0.f)) : 0xffffffffu;
+          const unsigned mn = __reduce_min_sync(FULL, key);
+          const int wl = __ffs(__ballot_sync(FULL, push && key == mn)) - 1;
+          const int last = 31 - __clz(pm);
+          if (c.lane == wl) pos = __popc(pm) - 1;
+          else if (c.lane == last) pos = __popc(pm & ((1u << wl) - 1u));
+        }
+        if (push) {
+          const int s2 = top + pos;
+          c.st[F_POSE * kStack + s2] = pose;
+          c.st[F_TA * kStack + s2] = cta;
+          c.st[F_TB * kStack + s2] = ctb;
+          #pragma unroll
+          for (int q = 0; q < 6; ++q) {
+            c.st[(F_BA + q) * kStack + s2] = (uint32_t)CA[q];
+            c.st[(F_BB + q) * kStack + s2] = (uint32_t)CB[q];
+          }
+          if (MODE == 1) c.st[F_LB * kStack + s2] = __float_as_uint(lb);
+        }
+        top += __popc(pm);
       }
       // ---- leaf pairs into the leaf queue
       const unsigned lm = __ballot_sync(FULL, leafpair);
       if (lm) {
         if (leafpair) {
-          int s2 = w.nleaf + __popc(lm & lt);
-          w.lq[0 * kLeafQ + s2] = pose;
-          w.lq[1 * kLeafQ + s2] = cta;
-          w.lq[2 * kLeafQ + s2] = ctb;
+          const int s2 = nleaf + __popc(lm & lt);
+          c.lq[0 * kLeafQ + s2] = pose;
+          c.lq[1 * kLeafQ + s2] = cta;
+          c.lq[2 * kLeafQ + s2] = ctb;
         }
-        w.nleaf += __popc(lm);
+        nleaf += __popc(lm);
+        if (STATS) s_leaf += __popc(lm);
       }
       __syncwarp();
-      if (w.nleaf > kLeafQ - 32) drain_leaves<MODE, STATS>(p, w);
+      if (nleaf > kLeafQ - 32) {
+        s_tri += drain_leaves<MODE>(p, c, nleaf);
+        nleaf = 0;
+      }
     }
   }
-  if (w.nleaf > 0) drain_leaves<MODE, STATS>(p, w);
-  if (STATS && w.lane == 0) {
-    atomicAdd(&p.ctl->stats[0], w.s_bv);
-    atomicAdd(&p.ctl->stats[1], w.s_exp);
-    atomicAdd(&p.ctl->stats[2], w.s_leaf);
-    atomicAdd(&p.ctl->stats[3], w.s_tri);
-    atomicAdd(&p.ctl->stats[6], w.s_tri * 72ull);
-    atomicAdd(&p.ctl->stats[7], w.s_spill);
-  }
+  if (nleaf > 0) s_tri += drain_leaves<MODE>(p, c, nleaf);
   if (STATS) {
-    // nodes decoded: summed over lanes
-    unsigned long long d = w.s_dec;
+    unsigned long long d = s_dec, r = s_rec;
     #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) d += __shfl_down_sync(FULL, d, o);
-    if (w.lane == 0) atomicAdd(&p.ctl->stats[4], d);
+    for (int o = 16; o > 0; o >>= 1) {
+      d += __shfl_down_sync(FULL, d, o);
+      r += __shfl_down_sync(FULL, r, o);
+    }
+    if (c.lane == 0) {
+      atomicAdd(&p.ctl->stats[0], s_bv);
+      atomicAdd(&p.ctl->stats[1], s_exp);
+      atomicAdd(&p.ctl->stats[2], s_leaf);
+      atomicAdd(&p.ctl->stats[3], s_tri);
+      atomicAdd(&p.ctl->stats[4], d);
+      atomicAdd(&p.ctl->stats[5], r);
+      atomicAdd(&p.ctl->stats[6], s_tri * 72ull);
+      atomicAdd(&p.ctl->stats[7], s_spill);
+    }
   }
 }
 

@@ -1,0 +1,205 @@
+// leaf_geometry.cuh — checkPrimitives for the device: Möller's
+// triangle–triangle interval test for closed triangles and the
+// exact triangle–triangle distance, templated on the scalar type
+// so the distance variant can re-evaluate near-contact candidates in fp64.
+#pragma once
+
+#include <cfloat>
+
+namespace cbvh {
+
+template <class F>
+struct TriT {
+  F v[3][3];
+};
+
+__device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float div_(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double div_(double a, double b) { return a / b; }
+__device__ __forceinline__ float sqrt_(float a) { return sqrtf(a); }
+__device__ __forceinline__ double sqrt_(double a) { return sqrt(a); }
+__device__ __forceinline__ float clamp01(float a) { return __saturatef(a); }
+__device__ __forceinline__ double clamp01(double a) { return fmin(1.0, fmax(0.0, a)); }
+
+template <class F>
+__device__ __forceinline__ void vsub(const F* a, const F* b, F* r) {
+  r[0] = a[0] - b[0]; r[1] = a[1] - b[1]; r[2] = a[2] - b[2];
+}
+template <class F>
+__device__ __forceinline__ F vdot(const F* a, const F* b) {
+  return fma_(a[0], b[0], fma_(a[1], b[1], a[2] * b[2]));
+}
+template <class F>
+__device__ __forceinline__ void vcross(const F* a, const F* b, F* r) {
+  r[0] = a[1] * b[2] - a[2] * b[1];
+  r[1] = a[2] * b[0] - a[0] * b[2];
+  r[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+template <class F>
+__device__ __forceinline__ F orient2(const F* a, const F* b, const F* c) {
+  return (b[0] - a[0]) * (c[1] - a[1]) - (b[1] - a[1]) * (c[0] - a[0]);
+}
+
+// closed 2-D segment intersection (touching counts)
+template <class F>
+__device__ bool seg2_intersect(const F* p1, const F* p2, const F* q1, const F* q2) {
+  F d1 = orient2(q1, q2, p1), d2 = orient2(q1, q2, p2);
+  F d3 = orient2(p1, p2, q1), d4 = orient2(p1, p2, q2);
+  if (((d1 > 0 && d2 < 0) || (d1 < 0 && d2 > 0)) && ((d3 > 0 && d4 < 0) || (d3 < 0 && d4 > 0))) return true;
+  auto on = [](const F* a, const F* b, const F* c) {
+    return fmin(a[0], b[0]) <= c[0] && c[0] <= fmax(a[0], b[0]) && fmin(a[1], b[1]) <= c[1] &&
+           c[1] <= fmax(a[1], b[1]);
+  };
+  return (d1 == 0 && on(q1, q2, p1)) || (d2 == 0 && on(q1, q2, p2)) || (d3 == 0 && on(p1, p2, q1)) ||
+         (d4 == 0 && on(p1, p2, q2));
+}
+
+template <class F>
+__device__ bool pt_in_tri2(const F* p, const F* a, const F* b, const F* c) {
+  F o1 = orient2(a, b, p), o2 = orient2(b, c, p), o3 = orient2(c, a, p);
+  bool neg = (o1 < 0) || (o2 < 0) || (o3 < 0);
+  bool pos = (o1 > 0) || (o2 > 0) || (o3 > 0);
+  return !(neg && pos);
+}
+
+// coplanar triangles: project on the plane dropping the normal's dominant axis
+template <class F>
+__device__ __noinline__ bool coplanar2(const F* N, const TriT<F>& V, const TriT<F>& U) {
+  F a0 = fabs(N[0]), a1 = fabs(N[1]), a2 = fabs(N[2]);
+  int i0, i1;
+  if (a0 >= a1 && a0 >= a2) { i0 = 1; i1 = 2; }
+  else if (a1 >= a2) { i0 = 0; i1 = 2; }
+  else { i0 = 0; i1 = 1; }
+  F v[3][2], u[3][2];
+  for (int k = 0; k < 3; ++k) {
+    v[k][0] = V.v[k][i0]; v[k][1] = V.v[k][i1];
+    u[k][0] = U.v[k][i0]; u[k][1] = U.v[k][i1];
+  }
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (seg2_intersect(v[i], v[(i + 1) % 3], u[j], u[(j + 1) % 3])) return true;
+  return pt_in_tri2(v[0], u[0], u[1], u[2]) || pt_in_tri2(u[0], v[0], v[1], v[2]);
+}
+
+// Möller 1997: the interval a triangle cuts on the line of the two planes,
+// from the projections p[] of its vertices and their plane distances d[]
+// (k = the vertex alone on its side).
+template <class F>
+__device__ __forceinline__ bool interval(const F p[3], const F d[3], F* t0, F* t1) {
+  int k, i, j;
+  if (d[0] * d[1] > 0) { k = 2; i = 0; j = 1; }
+  else if (d[0] * d[2] > 0) { k = 1; i = 0; j = 2; }
+  else if (d[1] * d[2] > 0 || d[0] != 0) { k = 0; i = 1; j = 2; }
+  else if (d[1] != 0) { k = 1; i = 0; j = 2; }
+  else if (d[2] != 0) { k = 2; i = 0; j = 1; }
+  else return false;
+  F a = p[k] + (p[i] - p[k]) * div_(d[k], d[k] - d[i]);
+  F b = p[k] + (p[j] - p[k]) * div_(d[k], d[k] - d[j]);
+  *t0 = fmin(a, b);
+  *t1 = fmax(a, b);
+  return true;
+}
+
+template <class F>
+__device__ bool tri_tri_overlap(const TriT<F>& V, const TriT<F>& U) {
+  F e1[3], e2[3], N1[3], N2[3];
+  vsub(V.v[1], V.v[0], e1); vsub(V.v[2], V.v[0], e2); vcross(e1, e2, N1);
+  F d1 = -vdot(N1, V.v[0]);
+  F du[3] = {vdot(N1, U.v[0]) + d1, vdot(N1, U.v[1]) + d1, vdot(N1, U.v[2]) + d1};
+  if ((du[0] > 0 && du[1] > 0 && du[2] > 0) || (du[0] < 0 && du[1] < 0 && du[2] < 0)) return false;
+  vsub(U.v[1], U.v[0], e1); vsub(U.v[2], U.v[0], e2); vcross(e1, e2, N2);
+  F d2 = -vdot(N2, U.v[0]);
+  F dv[3] = {vdot(N2, V.v[0]) + d2, vdot(N2, V.v[1]) + d2, vdot(N2, V.v[2]) + d2};
+  if ((dv[0] > 0 && dv[1] > 0 && dv[2] > 0) || (dv[0] < 0 && dv[1] < 0 && dv[2] < 0)) return false;
+  if (du[0] == 0 && du[1] == 0 && du[2] == 0) return coplanar2(N1, V, U);
+  F D[3];
+  vcross(N1, N2, D);
+  int ax = 0;
+  F m = fabs(D[0]);
+  if (fabs(D[1]) > m) { m = fabs(D[1]); ax = 1; }
+  if (fabs(D[2]) > m) { m = fabs(D[2]); ax = 2; }
+  if (m == 0) return coplanar2(N1, V, U);
+  F vp[3] = {V.v[0][ax], V.v[1][ax], V.v[2][ax]};
+  F up[3] = {U.v[0][ax], U.v[1][ax], U.v[2][ax]};
+  F a0, a1, b0, b1;
+  if (!interval(vp, dv, &a0, &a1) || !interval(up, du, &b0, &b1)) return coplanar2(N1, V, U);
+  return !(a1 < b0 || b1 < a0);
+}
+
+template <class F>
+__device__ __forceinline__ F pt_seg_d2(const F* p, const F* a, const F* b) {
+  F ab[3], ap[3];
+  vsub(b, a, ab); vsub(p, a, ap);
+  F L = vdot(ab, ab);
+  F t = L > 0 ? clamp01(vdot(ap, ab) / L) : F(0);
+  F q[3] = {fma_(t, ab[0], a[0]) - p[0], fma_(t, ab[1], a[1]) - p[1], fma_(t, ab[2], a[2]) - p[2]};
+  return vdot(q, q);
+}
+
+// min over (s,t) in [0,1]^2: the stationary point when inside, else the four
+// boundary point–segment distances; every candidate is a real pair of points,
+// so rounding can only over-estimate the minimum.
+template <class F>
+__device__ F seg_seg_d2(const F* p0, const F* p1, const F* q0, const F* q1) {
+  F best = fmin(fmin(pt_seg_d2(p0, q0, q1), pt_seg_d2(p1, q0, q1)), fmin(pt_seg_d2(q0, p0, p1), pt_seg_d2(q1, p0, p1)));
+  F d1[3], d2[3], r[3];
+  vsub(p1, p0, d1); vsub(q1, q0, d2); vsub(p0, q0, r);
+  F a = vdot(d1, d1), e = vdot(d2, d2), b = vdot(d1, d2), c = vdot(d1, r), f = vdot(d2, r);
+  F den = a * e - b * b;
+  if (den > 0) {
+    F s = (b * f - c * e) / den, t = (a * f - b * c) / den;
+    if (s >= 0 && s <= 1 && t >= 0 && t <= 1) {
+      F w[3] = {r[0] + s * d1[0] - t * d2[0], r[1] + s * d1[1] - t * d2[1], r[2] + s * d1[2] - t * d2[2]};
+      best = fmin(best, vdot(w, w));
+    }
+  }
+  return best;
+}
+
+// point–triangle: the plane distance when the projection lies inside the
+// closed triangle, else the nearest edge
+template <class F>
+__device__ F pt_tri_d2(const F* p, const TriT<F>& T) {
+  F e1[3], e2[3], n[3], w[3];
+  vsub(T.v[1], T.v[0], e1); vsub(T.v[2], T.v[0], e2); vcross(e1, e2, n);
+  F best = fmin(fmin(pt_seg_d2(p, T.v[0], T.v[1]), pt_seg_d2(p, T.v[1], T.v[2])), pt_seg_d2(p, T.v[2], T.v[0]));
+  F nn = vdot(n, n);
+  if (nn > 0) {
+    vsub(p, T.v[0], w);
+    F h = vdot(w, n) / nn;
+    F q[3] = {p[0] - h * n[0], p[1] - h * n[1], p[2] - h * n[2]};
+    F a[3], b[3], c0[3];
+    vsub(T.v[1], T.v[0], a); vsub(q, T.v[0], b); vcross(a, b, c0);
+    bool in = vdot(c0, n) >= 0;
+    vsub(T.v[2], T.v[1], a); vsub(q, T.v[1], b); vcross(a, b, c0);
+    in = in && vdot(c0, n) >= 0;
+    vsub(T.v[0], T.v[2], a); vsub(q, T.v[2], b); vcross(a, b, c0);
+    in = in && vdot(c0, n) >= 0;
+    if (in) {
+      F d = p[0] - q[0], e = p[1] - q[1], f = p[2] - q[2];
+      best = fmin(best, d * d + e * e + f * f);
+    }
+  }
+  return best;
+}
+
+template <class F>
+__device__ F tri_tri_dist(const TriT<F>& V, const TriT<F>& U) {
+  if (tri_tri_overlap(V, U)) return F(0);
+  F best = F(FLT_MAX);
+  #pragma unroll 1
+  for (int k = 0; k < 3; ++k) {
+    best = fmin(best, pt_tri_d2(V.v[k], U));
+    best = fmin(best, pt_tri_d2(U.v[k], V));
+  }
+  #pragma unroll 1
+  for (int i = 0; i < 3; ++i)
+    #pragma unroll 1
+    for (int j = 0; j < 3; ++j)
+      best = fmin(best, seg_seg_d2(V.v[i], V.v[(i + 1) % 3], U.v[j], U.v[(j + 1) % 3]));
+  return sqrt_(best);
+}
+
+}  // namespace cbvh
