@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: collide_batch over BASELINE.json's largest
+config (config 5, "large planning batch": 1,048,576 poses, A = 100k-triangle
+noisy sphere, B = 1,024 blobs / 4.06M triangles, 4-ary BVHs, 8-bit corrections,
+64-node treelets) on N GPUs of one node.
+
+One step = one collide_batch call over the rank's whole pose batch (all §8(a)
+rows: pose setup, work acquisition, treelet fetch + decode, SAT child-pair
+tests, compaction, leaf Möller tests, outputs).  Blobs and poses are resident
+in HBM before the timed region; L2 is flushed (256 MiB write) between timed
+steps, outside the CUDA events.  Multi-GPU: one process per GPU (torchrun),
+each rank processes its own batch of the same size (weak scaling, no data-path
+collective); the step time is the max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from workloads import generators as G  # noqa: E402
+
+METRIC = "collision queries (poses)/sec"
+UNIT = "poses/s"
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["_source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    return {"hbm_gbs": 6650.0, "_source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.3)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for nm, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        # median under load: samples within the top half of observed clocks
+        loaded = [x for x in sm if sm and x >= 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def cpu_oracle_rate(w, n_sample: int, nthreads: int = 0, budget_s: float = 25.0):
+    """The fp64 oracle (as it stands) on a bounded prefix of the workload's poses."""
+    import oracle as O
+    t0 = time.time()
+    tA = O.Tree.from_mesh(w.A.vertices, w.A.triangles)
+    tB = O.Tree.from_mesh(w.B.vertices, w.B.triangles)
+    build_s = time.time() - t0
+    delta = O.band_delta(w.A.vertices)
+    cores = nthreads or os.cpu_count()
+    # grow the sample until ~budget_s of oracle time (bounded by n_sample)
+    n, done, el = 64, 0, 0.0
+    while True:
+        P = w.poses[done:done + n]
+        t = time.time()
+        O.collide(tA, tB, P, delta, nthreads)
+        el += time.time() - t
+        done += len(P)
+        if el > budget_s or done >= n_sample:
+            break
+        n = min(n_sample - done, max(64, int(len(P) * max(1.0, (budget_s - el) / max(el, 1e-3)) * 0.5)))
+    return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {done} of {len(w.poses)} poses of {w.name}, fp64 oracle with "
+                      f"std::thread x {cores}; oracle BVH build {build_s:.1f} s not timed",
+            "seconds": el}
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, same config/metric."""
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return
+    w = G.make_config(args.config)
+    import oracle as O
+    tA = O.Tree.from_mesh(w.A.vertices, w.A.triangles)
+    tB = O.Tree.from_mesh(w.B.vertices, w.B.triangles)
+    delta = O.band_delta(w.A.vertices)
+    per_step = args.ref_poses
+    times = []
+    for s in range(args.warmup + args.steps):
+        lo = (s * per_step) % len(w.poses)
+        P = w.poses[lo:lo + per_step]
+        t = time.time()
+        O.collide(tA, tB, P, delta, 0)
+        dt = time.time() - t
+        if s >= args.warmup:
+            times.append(dt)
+    T = sum(times)
+    value = per_step * args.steps / T
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": w.name, "poses_per_step": per_step,
+                                            "sample": "consecutive pose windows of the config-5 batch"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} poses per step x {args.steps} steps"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run(args):
+    import torch
+    import paper_2012_05348_b200 as M
+    from paper_2012_05348_b200 import _lib as L
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    w = G.make_config(args.config, num_poses=args.poses, pose_seed_offset=rank)
+    N = len(w.poses)
+    t0 = time.time()
+    A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, w.leaf)
+    B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, w.leaf)
+    build_s = time.time() - t0
+    A.to_device(dev)
+    B.to_device(dev)
+    poses_h = torch.from_numpy(w.poses).pin_memory()
+    poses = poses_h.to(dev)
+    hit = torch.empty(N, dtype=torch.uint8, device=dev)
+    cnt = torch.empty(N, dtype=torch.int32, device=dev)
+    ws = M.Workspace(A, B, 0, dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    lib = L.load()
+
+    def step():
+        M.collide_batch(A, B, poses, hit, cnt, ws)
+
+    # ---- warm-up (untimed)
+    for _ in range(max(3, args.warmup)):
+        step()
+    M.check(ws)
+
+    # ---- timed region: K steps, per-step CUDA events, L2 flushed between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 255)
+            ev[k][0].record(stream)
+            lib.cbvh_set_kernel_events(kev[k][0].cuda_event, kev[k][1].cuda_event)
+            step()
+            launches += M.last_launch_count()
+            ev[k][1].record(stream)
+        lib.cbvh_set_kernel_events(None, None)
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    M.check(ws)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    kern_ms = [a.elapsed_time(b) for a, b in kev]
+    T = sum(step_ms) / 1e3
+    if dist:
+        t = torch.tensor([T], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        T = float(t.item())
+    value = N * args.steps * world / T
+    hits = int(hit.sum().item())
+
+    # ---- stats run (untimed): BV-pair tests and algorithmic bytes per launch
+    M.collide_batch(A, B, poses, hit, cnt, ws, stats=True)
+    st = M.read_stats(ws)
+    kern_s = statistics.mean(kern_ms) / 1e3
+    alg_bytes = st["record_bytes"] + st["tri_bytes"] + N * (48 + 5)
+    peaks = measured_peaks()
+    achieved = alg_bytes / kern_s / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(f"cfg{args.config}", {}).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    # ---- end-to-end through the public API with host buffers (pinned)
+    hit_h = torch.empty(N, dtype=torch.uint8, pin_memory=True)
+    cnt_h = torch.empty(N, dtype=torch.int32, pin_memory=True)
+    e2e_ms = []
+    for k in range(args.warmup + args.steps):
+        flush.fill_(k & 255)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        poses.copy_(poses_h, non_blocking=True)
+        M.collide_batch(A, B, poses, hit, cnt, ws)
+        hit_h.copy_(hit, non_blocking=True)
+        cnt_h.copy_(cnt, non_blocking=True)
+        b.record(stream)
+        b.synchronize()
+        if k >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b))
+    E = sum(e2e_ms) / 1e3
+    if dist:
+        t = torch.tensor([E], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        E = float(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_oracle_rate(w, n_sample=args.cpu_poses, budget_s=args.cpu_budget)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": w.name, "poses_per_gpu": N, "A_tris": w.A.num_triangles,
+                       "B_tris": w.B.num_triangles, "branching": w.branching, "bits": w.bits,
+                       "treelet_nodes": w.treelet, "leaf_size": w.leaf,
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "parallelism": f"pose-sharded x{world} (independent batches)"},
+            "bv_pair_tests_per_s": st["bv_tests"] / (statistics.median(step_ms) / 1e3),
+            "bv_pair_tests_per_step": st["bv_tests"],
+            "hit_fraction": hits / N,
+            "bytes_per_node": {"A": A.info["bytes_per_node"], "B": B.info["bytes_per_node"]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                         "kernel": "traverse_kernel<collide>", "kernel_ms": 1e3 * kern_s,
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "peak_source": peaks["_source"] + " hbm_gbs (copy bandwidth)"},
+            "stats": st,
+            "e2e": {"value": N * args.steps * world / E, "unit": UNIT,
+                    "h2d_bytes_per_step": int(poses_h.numel() * 4),
+                    "d2h_bytes_per_step": int(N * (1 + 4))},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "build_s": build_s,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = {k: v for k, v in cpu.items() if k != "seconds"}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--poses", type=int, default=None, help="override the config's pose count")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
+    ap.add_argument("--cpu-poses", type=int, default=100000)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-poses", type=int, default=2048, help="poses per --impl reference step")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -148,8 +148,8 @@ typedef struct {
   uint64_t leaf_pairs;      /* (leafA, leafB) pairs reaching checkPrimitives */
   uint64_t tri_tests;       /* triangle-pair tests */
   uint64_t nodes_decoded;   /* child boxes decoded (records fetched) */
-  uint64_t record_bytes;    /* compressed bytes of those records (topo + codes) */
-  uint64_t tri_bytes;       /* triangle bytes read by the leaf phase */
+  uint64_t record_bytes;    /* compressed bytes of those records (4 B topo + 6w/8 B codes each) */
+  uint64_t tri_bytes;       /* algorithmic triangle bytes: (c_A + c_B) x 36 B per leaf pair */
   uint64_t spills;          /* stack spill events */
 } cbvh_stats;
 
@@ -170,6 +170,12 @@ int cbvh_read_stats(const void* d_ws, cbvh_stats* out, void* stream);
 /* Number of kernel launches the last collide_batch/distance_batch issued on
  * this thread (for the bench's gpu_launches count). */
 int cbvh_last_launch_count(void);
+
+/* Observability: when non-null, the next collide/distance calls on this
+ * thread record `start` (cudaEvent_t) just before the traversal kernel and
+ * `stop` just after it, on the call's stream — used by bench.py to time the
+ * dominant kernel alone.  Pass nulls to disable. */
+void cbvh_set_kernel_events(void* start, void* stop);
 
 /* Thread-local message for the last non-zero status. */
 const char* cbvh_last_error(void);

@@ -57,7 +57,7 @@ class cbvh_stats(C.Structure):
 EXPORTS = ("build_compressed_bvh", "cbvh_free_blob", "cbvh_blob_info", "cbvh_bind",
            "cbvh_workspace_bytes", "collide_batch", "distance_batch", "collide_batch_stats",
            "distance_batch_stats", "cbvh_check", "cbvh_read_stats", "cbvh_last_launch_count",
-           "cbvh_last_error")
+           "cbvh_last_error", "cbvh_set_kernel_events")
 
 _lib = None
 
@@ -99,6 +99,8 @@ def load():
     L.cbvh_read_stats.restype = C.c_int
     L.cbvh_last_launch_count.argtypes = []
     L.cbvh_last_launch_count.restype = C.c_int
+    L.cbvh_set_kernel_events.argtypes = [C.c_void_p, C.c_void_p]
+    L.cbvh_set_kernel_events.restype = None
     L.cbvh_last_error.argtypes = []
     L.cbvh_last_error.restype = C.c_char_p
     _lib = L

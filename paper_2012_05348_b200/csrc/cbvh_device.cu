@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_cons
   c.lq = c.st + kFields * kStack;
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * kFields;
   int top = 0, nleaf = 0, spill_top = 0;
-  unsigned long long s_bv = 0, s_exp = 0, s_leaf = 0, s_tri = 0, s_dec = 0, s_rec = 0, s_spill = 0;
+  unsigned long long s_bv = 0, s_exp = 0, s_leaf = 0, s_tri = 0, s_dec = 0, s_rec = 0, s_lbytes = 0, s_spill = 0;
   bool poses_left = true;
   const unsigned lt = lanemask_lt();
   const float scale_ab = p.A.maxabs + p.B.maxabs;
@@ -400,7 +400,9 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_cons
 
   while (true) {
     // ---- acquire poses when the stack runs low: push their root pairs
-    if (poses_left && top < kLowWater) {
+    // (only when nothing is spilled: spilled items are finished first, which
+    // bounds the stack by the deepest single traversal, not the batch size)
+    if (poses_left && top < kLowWater && spill_top == 0) {
       unsigned base = 0;
       if (c.lane == 0) base = atomicAdd(&p.ctl->cursor, (unsigned)kGrab);
       base = __shfl_sync(FULL, base, 0);
@@ -584,22 +586,32 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_cons
           c.lq[2 * kLeafQ + s2] = ctb;
         }
         nleaf += __popc(lm);
-        if (STATS) s_leaf += __popc(lm);
+        if (STATS) {
+          s_leaf += __popc(lm) * (c.lane == 0 ? 1 : 0);
+          if (leafpair) s_lbytes += 36u * (((cta >> 29) & 3u) + ((ctb >> 29) & 3u) + 2u);
+        }
       }
       __syncwarp();
-      if (nleaf > kLeafQ - 32) {
+      // collide: drain in full rounds; distance: drain promptly so that the
+      // pose's best distance tightens and prunes the rest of the traversal
+      if (nleaf > kLeafQ - 32 || (MODE == 1 && nleaf >= 2)) {
         s_tri += drain_leaves<MODE>(p, c, nleaf);
         nleaf = 0;
       }
     }
+    if (MODE == 1 && nleaf > 0 && top == 0) {
+      s_tri += drain_leaves<MODE>(p, c, nleaf);
+      nleaf = 0;
+    }
   }
   if (nleaf > 0) s_tri += drain_leaves<MODE>(p, c, nleaf);
   if (STATS) {
-    unsigned long long d = s_dec, r = s_rec;
+    unsigned long long d = s_dec, r = s_rec, lb = s_lbytes;
     #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       d += __shfl_down_sync(FULL, d, o);
       r += __shfl_down_sync(FULL, r, o);
+      lb += __shfl_down_sync(FULL, lb, o);
     }
     if (c.lane == 0) {
       atomicAdd(&p.ctl->stats[0], s_bv);
@@ -608,7 +620,7 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_cons
       atomicAdd(&p.ctl->stats[3], s_tri);
       atomicAdd(&p.ctl->stats[4], d);
       atomicAdd(&p.ctl->stats[5], r);
-      atomicAdd(&p.ctl->stats[6], s_tri * 72ull);
+      atomicAdd(&p.ctl->stats[6], lb);
       atomicAdd(&p.ctl->stats[7], s_spill);
     }
   }
@@ -636,6 +648,7 @@ __global__ void init_kernel(Params p, int reset_stats) {
 
 static thread_local char g_err[512] = "";
 static thread_local int g_launches = 0;
+static thread_local cudaEvent_t g_ev_start = nullptr, g_ev_stop = nullptr;
 
 int set_error(int code, const char* msg) {
   std::snprintf(g_err, sizeof g_err, "%s", msg);
@@ -741,8 +754,10 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "init_kernel launch");
   if (N == 0) return CBVH_OK;
+  if (g_ev_start) cudaEventRecord(g_ev_start, st);
   traverse_kernel<MODE, STATS><<<s.blocks, kWarps * 32, smem_bytes(), st>>>(p);
   g_launches++;
+  if (g_ev_stop) cudaEventRecord(g_ev_stop, st);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "traverse_kernel launch");
   return CBVH_OK;
@@ -755,6 +770,11 @@ using namespace cbvh;
 extern "C" {
 
 const char* cbvh_last_error(void) { return g_err; }
+
+void cbvh_set_kernel_events(void* start, void* stop) {
+  g_ev_start = static_cast<cudaEvent_t>(start);
+  g_ev_stop = static_cast<cudaEvent_t>(stop);
+}
 int cbvh_last_launch_count(void) { return g_launches; }
 
 int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh* out) {

@@ -149,12 +149,13 @@ def test_self_identity_and_far(M, cfg1):
     P[1, 3] = 10.0
     P[2, 7] = -3.0
     hit, gc = run_collide(M, A, A, P)
-    pairs = O.collide_pairs(O.Tree.from_mesh(w.A.vertices, w.A.triangles),
-                            O.Tree.from_mesh(w.A.vertices, w.A.triangles), P[0])
-    # coincident geometry: every pair is a band pair (pen = 0), count must
-    # cover at least the triangles meeting themselves and at most all touching pairs
-    assert w.A.num_triangles <= gc[0] <= len(pairs)
-    assert gc[1] == 0 and gc[2] == 0 and hit[0] == 1
+    tA = O.Tree.from_mesh(w.A.vertices, w.A.triangles)
+    _, H, Z, _ = O.collide(tA, tA, P, O.band_delta(w.A.vertices))
+    check_collide(hit, gc, H, Z, "self")
+    # coincident geometry: every touching pair is a band pair (pen = 0); each
+    # triangle meets itself exactly (identical fp32 coordinates, coplanar test)
+    assert gc[0] >= w.A.num_triangles and hit[0] == 1
+    assert gc[1] == 0 and gc[2] == 0
 
 
 def test_empty_and_ragged_batches(M, cfg1):
