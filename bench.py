@@ -212,6 +212,9 @@ def run(args):
     # ---- timed region: K steps, per-step CUDA events, L2 flushed between steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in kev:  # torch creates the underlying cudaEvent_t lazily, on first record
+        a.record(stream)
+        b.record(stream)
     launches = 0
     if dist:
         dist.barrier()

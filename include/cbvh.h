@@ -38,7 +38,7 @@ extern "C" {
 
 enum {
   CBVH_OK = 0,
-  CBVH_EINVAL = -1,     /* bad argument: B not in {2,4,8}, bits not in [2,16], T < B, c not in [1,4], N < 0, null ptr */
+  CBVH_EINVAL = -1,     /* bad argument: B not in {2,4,8}, bits not in [2,16], T < B, c not in [1,4], N not in [0, 2^30), null ptr */
   CBVH_EMESH = -2,      /* empty mesh, index out of range, non-finite vertex, too many triangles (> 2^29) */
   CBVH_EBLOB = -3,      /* bad magic / version / size / section offsets */
   CBVH_ECUDA = -4,      /* a CUDA runtime call failed (message in cbvh_last_error) */
@@ -140,6 +140,29 @@ int collide_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
  * pose i (0 when any pair intersects), fp32.  Arguments as collide_batch. */
 int distance_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N,
                    float* d_min_dist, void* d_ws, size_t ws_bytes, void* stream);
+
+/* Query options (nullable everywhere; null = defaults). */
+enum {
+  /* Descend only the node whose box is larger (sum of extents) when both
+   * are internal; Alg. 1's other cases unchanged.  Same result, far fewer
+   * BV tests when the models differ in scale.  Default. */
+  CBVH_DESCENT_LARGER = 1,
+  /* Alg. 1 verbatim: descend both nodes, test the cross product
+   * of their children. */
+  CBVH_DESCENT_SIMULTANEOUS = 0
+};
+typedef struct {
+  int descent; /* CBVH_DESCENT_* */
+  int stats;   /* non-zero: accumulate cbvh_stats in the workspace (slower) */
+} cbvh_query_opts;
+
+/* collide_batch / distance_batch with options (opts may be null). */
+int collide_batch_ex(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N,
+                     uint8_t* d_hit, uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream,
+                     const cbvh_query_opts* opts);
+int distance_batch_ex(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N,
+                      float* d_min_dist, void* d_ws, size_t ws_bytes, void* stream,
+                      const cbvh_query_opts* opts);
 
 /* Stats counters gathered by the *_stats variants. */
 typedef struct {

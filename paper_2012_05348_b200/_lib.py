@@ -54,10 +54,18 @@ class cbvh_stats(C.Structure):
                 ("tri_bytes", C.c_uint64), ("spills", C.c_uint64)]
 
 
+class cbvh_query_opts(C.Structure):
+    _fields_ = [("descent", C.c_int), ("stats", C.c_int)]
+
+
+CBVH_DESCENT_SIMULTANEOUS, CBVH_DESCENT_LARGER = 0, 1
+DESCENT = {"simultaneous": CBVH_DESCENT_SIMULTANEOUS, "alg1": CBVH_DESCENT_SIMULTANEOUS,
+           "larger": CBVH_DESCENT_LARGER}
+
 EXPORTS = ("build_compressed_bvh", "cbvh_free_blob", "cbvh_blob_info", "cbvh_bind",
            "cbvh_workspace_bytes", "collide_batch", "distance_batch", "collide_batch_stats",
            "distance_batch_stats", "cbvh_check", "cbvh_read_stats", "cbvh_last_launch_count",
-           "cbvh_last_error", "cbvh_set_kernel_events")
+           "cbvh_last_error", "cbvh_set_kernel_events", "collide_batch_ex", "distance_batch_ex")
 
 _lib = None
 
@@ -93,6 +101,12 @@ def load():
         f.argtypes = [P(cbvh_bvh), P(cbvh_bvh), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                       C.c_size_t, C.c_void_p]
         f.restype = C.c_int
+    L.collide_batch_ex.argtypes = [P(cbvh_bvh), P(cbvh_bvh), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_size_t, C.c_void_p, P(cbvh_query_opts)]
+    L.collide_batch_ex.restype = C.c_int
+    L.distance_batch_ex.argtypes = [P(cbvh_bvh), P(cbvh_bvh), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                    C.c_size_t, C.c_void_p, P(cbvh_query_opts)]
+    L.distance_batch_ex.restype = C.c_int
     L.cbvh_check.argtypes = [C.c_void_p, C.c_void_p]
     L.cbvh_check.restype = C.c_int
     L.cbvh_read_stats.argtypes = [C.c_void_p, P(cbvh_stats), C.c_void_p]

@@ -114,9 +114,19 @@ def _check_poses(poses):
     return int(poses.shape[0])
 
 
+def _opts(descent: str, stats: bool) -> L.cbvh_query_opts:
+    if descent not in L.DESCENT:
+        raise ValueError(f"descent must be one of {sorted(L.DESCENT)}")
+    return L.cbvh_query_opts(L.DESCENT[descent], 1 if stats else 0)
+
+
 def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=None,
-                  workspace: Workspace | None = None, stream=None, stats: bool = False):
-    """C-ABI collide_batch: per-pose hit flag (uint8) and colliding pair count (int32 view of uint32)."""
+                  workspace: Workspace | None = None, stream=None, stats: bool = False,
+                  descent: str = "larger"):
+    """C-ABI collide_batch: per-pose hit flag (uint8) and colliding pair count (int32 view of uint32).
+
+    descent: "larger" (default: descend the node with the larger box) or
+    "simultaneous" (Alg. 1 verbatim).  Both give identical results."""
     torch = _torch()
     N = _check_poses(poses)
     dev = poses.device
@@ -126,15 +136,17 @@ def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=Non
         count = torch.empty(N, dtype=torch.int32, device=dev)
     if workspace is None:
         workspace = Workspace(A, B, 0, dev)
-    f = L.load().collide_batch_stats if stats else L.load().collide_batch
-    L.check(f(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
-              C.c_void_p(hit.data_ptr()), C.c_void_p(count.data_ptr()), C.c_void_p(workspace.ptr),
-              workspace.nbytes, C.c_void_p(_stream_ptr(stream))))
+    o = _opts(descent, stats)
+    L.check(L.load().collide_batch_ex(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
+                                      C.c_void_p(hit.data_ptr()), C.c_void_p(count.data_ptr()),
+                                      C.c_void_p(workspace.ptr), workspace.nbytes,
+                                      C.c_void_p(_stream_ptr(stream)), C.byref(o)))
     return hit, count
 
 
 def distance_batch(A: CompressedBVH, B: CompressedBVH, poses, dist=None,
-                   workspace: Workspace | None = None, stream=None, stats: bool = False):
+                   workspace: Workspace | None = None, stream=None, stats: bool = False,
+                   descent: str = "larger"):
     """C-ABI distance_batch: per-pose minimum triangle–triangle distance (fp32)."""
     torch = _torch()
     N = _check_poses(poses)
@@ -142,10 +154,10 @@ def distance_batch(A: CompressedBVH, B: CompressedBVH, poses, dist=None,
         dist = torch.empty(N, dtype=torch.float32, device=poses.device)
     if workspace is None:
         workspace = Workspace(A, B, 1, poses.device)
-    f = L.load().distance_batch_stats if stats else L.load().distance_batch
-    L.check(f(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
-              C.c_void_p(dist.data_ptr()), C.c_void_p(workspace.ptr), workspace.nbytes,
-              C.c_void_p(_stream_ptr(stream))))
+    o = _opts(descent, stats)
+    L.check(L.load().distance_batch_ex(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
+                                       C.c_void_p(dist.data_ptr()), C.c_void_p(workspace.ptr), workspace.nbytes,
+                                       C.c_void_p(_stream_ptr(stream)), C.byref(o)))
     return dist
 
 

@@ -89,7 +89,13 @@ struct Params {
   uint32_t* dist_bits;   // float bits of the running minimum distance
   Control* ctl;
   uint32_t* spill;       // [num_warps][kSpillCap][kFields]
+  int descent;           // CBVH_DESCENT_SIMULTANEOUS (Alg. 1 verbatim) or CBVH_DESCENT_LARGER
 };
+
+// item pose word: bits 0..29 pose id, bit 30 = descend a, bit 31 = descend b
+constexpr uint32_t kPoseMask = 0x3FFFFFFFu;
+constexpr uint32_t kDescA = 0x40000000u;
+constexpr uint32_t kDescB = 0x80000000u;
 
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -224,23 +230,26 @@ __device__ __forceinline__ Tri to_local(const PoseF& P, const Tri& W) {
   return L;
 }
 
-// fp64 re-evaluation of a near-contact distance candidate:
-// the same inputs (fp32 A triangle, fp32 world B triangle, fp32 pose) lifted
-// exactly to fp64, so the result meets the 1e-5 relative tolerance at any d.
+// fp64 re-evaluation of a near-contact distance candidate,
+// in the world frame as the distance is defined: A's fp32
+// triangle mapped by the fp32 pose lifted exactly to fp64, B's fp32 triangle
+// as is.  (The fp32 path works in A's frame with R^T, whose ~1e-7
+// non-orthonormality is an absolute error that a 1e-5 relative bound cannot
+// absorb at small distances.)
 __device__ __noinline__ float tri_dist_fp64(const PoseF& P, const float* trisA, uint32_t ia,
                                             const float* trisB, uint32_t ib) {
   Tri64 a, b;
   #pragma unroll
-  for (int k = 0; k < 9; ++k) a.v[k / 3][k % 3] = (double)__ldg(trisA + 9ull * ia + k);
-  #pragma unroll
   for (int v = 0; v < 3; ++v) {
-    double d0 = (double)__ldg(trisB + 9ull * ib + 3 * v) - (double)P.t[0];
-    double d1 = (double)__ldg(trisB + 9ull * ib + 3 * v + 1) - (double)P.t[1];
-    double d2 = (double)__ldg(trisB + 9ull * ib + 3 * v + 2) - (double)P.t[2];
+    const double x0 = (double)__ldg(trisA + 9ull * ia + 3 * v);
+    const double x1 = (double)__ldg(trisA + 9ull * ia + 3 * v + 1);
+    const double x2 = (double)__ldg(trisA + 9ull * ia + 3 * v + 2);
     #pragma unroll
     for (int k = 0; k < 3; ++k)
-      b.v[v][k] = fma((double)P.R[0][k], d0, fma((double)P.R[1][k], d1, (double)P.R[2][k] * d2));
+      a.v[v][k] = fma((double)P.R[k][0], x0, fma((double)P.R[k][1], x1, fma((double)P.R[k][2], x2, (double)P.t[k])));
   }
+  #pragma unroll
+  for (int k = 0; k < 9; ++k) b.v[k / 3][k % 3] = (double)__ldg(trisB + 9ull * ib + k);
   return (float)tri_tri_dist(a, b);
 }
 
@@ -250,10 +259,25 @@ __device__ __noinline__ float tri_dist_fp64(const PoseF& P, const float* trisA, 
 
 constexpr int kWarpSmemWords = kFields * kStack + 3 * kLeafQ;
 
-__device__ __forceinline__ int pair_count(uint32_t ta, uint32_t tb) {
-  int na = (ta & kLeafBit) ? 1 : (int)((ta >> 28) & 7u) + 1;
-  int nb = (tb & kLeafBit) ? 1 : (int)((tb >> 28) & 7u) + 1;
+// child pairs of an item: Alg. 1 enumerates children of every side it
+// descends (flags chosen at push time, see descent_flags)
+__device__ __forceinline__ int pair_count(uint32_t pw, uint32_t ta, uint32_t tb) {
+  int na = (pw & kDescA) ? (int)((ta >> 28) & 7u) + 1 : 1;
+  int nb = (pw & kDescB) ? (int)((tb >> 28) & 7u) + 1 : 1;
   return na * nb;
+}
+
+// Which side(s) an internal pair (a, b) descends.  Alg. 1 descends
+// both when both are internal; the LARGER rule descends only the node with the
+// larger box (sum of extents, A-local vs world — rotation-invariant up to
+// sqrt 3), which visits the same leaf pairs (reading R15).
+__device__ __forceinline__ uint32_t descent_flags(int rule, uint32_t ta, uint32_t tb, const int32_t CA[6],
+                                                  const int32_t CB[6], float cellA, float cellB) {
+  const bool ai = !(ta & kLeafBit), bi = !(tb & kLeafBit);
+  if (!(ai && bi) || rule == 0) return (ai ? kDescA : 0u) | (bi ? kDescB : 0u);
+  const float ea = (float)((CA[3] - CA[0]) + (CA[4] - CA[1]) + (CA[5] - CA[2])) * cellA;
+  const float eb = (float)((CB[3] - CB[0]) + (CB[4] - CB[1]) + (CB[5] - CB[2])) * cellB;
+  return ea >= eb ? kDescA : kDescB;
 }
 
 __device__ __forceinline__ int tri_pair_count(uint32_t ta, uint32_t tb) {
@@ -418,7 +442,9 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_cons
             c.lq[2 * kLeafQ + slot] = p.B.root_topo;
           } else {
             const int slot = top + c.lane;
-            c.st[F_POSE * kStack + slot] = base + c.lane;
+            c.st[F_POSE * kStack + slot] =
+                (base + c.lane) | descent_flags(p.descent, p.A.root_topo, p.B.root_topo, p.A.root, p.B.root,
+                                                p.A.cell, p.B.cell);
             c.st[F_TA * kStack + slot] = p.A.root_topo;
             c.st[F_TB * kStack + slot] = p.B.root_topo;
             #pragma unroll
@@ -451,7 +477,7 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_cons
     int n = 0;
     if (c.lane < top) {
       const int slot = top - 1 - c.lane;
-      n = pair_count(c.st[F_TA * kStack + slot], c.st[F_TB * kStack + slot]);
+      n = pair_count(c.st[F_POSE * kStack + slot], c.st[F_TA * kStack + slot], c.st[F_TB * kStack + slot]);
     }
     int incl = n;
     #pragma unroll
@@ -475,7 +501,8 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_cons
     const int start_e = __shfl_sync(FULL, incl - n, e);
     // this lane's item, read before anything is pushed over it
     const int slot = top - 1 - e;
-    const uint32_t pose = c.st[F_POSE * kStack + slot];
+    const uint32_t pword = c.st[F_POSE * kStack + slot];
+    const uint32_t pose = pword & kPoseMask;
     const uint32_t ta = c.st[F_TA * kStack + slot];
     const uint32_t tb = c.st[F_TB * kStack + slot];
     int32_t BA[6], BB[6];
@@ -494,7 +521,7 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_cons
     const float eps = 2e-6f * (tmax + scale_ab);
     float best = FLT_MAX;
     if (MODE == 1) best = __uint_as_float(__ldcg(&p.dist_bits[pose]));
-    const bool a_int = !(ta & kLeafBit), b_int = !(tb & kLeafBit);
+    const bool a_int = (pword & kDescA) != 0, b_int = (pword & kDescB) != 0;  // sides descended
     const int nb = b_int ? (int)((tb >> 28) & 7u) + 1 : 1;
 
     for (int pass = 0; pass < passes; ++pass) {
@@ -564,7 +591,7 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_cons
         }
         if (push) {
           const int s2 = top + pos;
-          c.st[F_POSE * kStack + s2] = pose;
+          c.st[F_POSE * kStack + s2] = pose | descent_flags(p.descent, cta, ctb, CA, CB, p.A.cell, p.B.cell);
           c.st[F_TA * kStack + s2] = cta;
           c.st[F_TB * kStack + s2] = ctb;
           #pragma unroll
@@ -716,10 +743,12 @@ static DevTree make_tree(const cbvh_bvh* T) {
 
 template <int MODE, bool STATS>
 static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
-                  uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream) {
+                  uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream, int descent) {
   g_launches = 0;
   if (!A || !B || !d_ws) return set_error(CBVH_EINVAL, "null argument");
-  if (N < 0 || N > 0x7fffffffLL) return set_error(CBVH_EINVAL, "N out of range");
+  if (N < 0 || N > 0x3fffffffLL) return set_error(CBVH_EINVAL, "N out of range [0, 2^30)");
+  if (descent != CBVH_DESCENT_LARGER && descent != CBVH_DESCENT_SIMULTANEOUS)
+    return set_error(CBVH_EINVAL, "bad descent rule");
   if (N > 0 && !d_poses) return set_error(CBVH_EINVAL, "null poses");
   if (N > 0 && MODE == 0 && (!d_hit || !d_count)) return set_error(CBVH_EINVAL, "null outputs");
   if (N > 0 && MODE == 1 && !d_dist) return set_error(CBVH_EINVAL, "null outputs");
@@ -747,6 +776,7 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
   p.dist_bits = reinterpret_cast<uint32_t*>(d_dist);
   p.ctl = static_cast<Control*>(d_ws);
   p.spill = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + 256);
+  p.descent = descent;
   int ib = (int)((N + 255) / 256);
   ib = ib < 1 ? 1 : (ib > 4096 ? 4096 : ib);
   init_kernel<MODE><<<ib, 256, 0, st>>>(p, STATS ? 1 : 0);
@@ -824,21 +854,38 @@ size_t cbvh_workspace_bytes(const cbvh_bvh* A, const cbvh_bvh* B, int64_t N, int
   return workspace_for_warps(w);
 }
 
+static int opts_descent(const cbvh_query_opts* o) { return o ? o->descent : CBVH_DESCENT_LARGER; }
+static int opts_stats(const cbvh_query_opts* o) { return o ? o->stats : 0; }
+
+int collide_batch_ex(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
+                     uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream, const cbvh_query_opts* o) {
+  if (opts_stats(o))
+    return launch<0, true>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o));
+  return launch<0, false>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o));
+}
+int distance_batch_ex(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, float* d_min_dist,
+                      void* d_ws, size_t ws_bytes, void* stream, const cbvh_query_opts* o) {
+  if (opts_stats(o))
+    return launch<1, true>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o));
+  return launch<1, false>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o));
+}
 int collide_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                   uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream) {
-  return launch<0, false>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream);
+  return collide_batch_ex(A, B, d_poses, N, d_hit, d_pair_count, d_ws, ws_bytes, stream, nullptr);
 }
 int collide_batch_stats(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                         uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream) {
-  return launch<0, true>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream);
+  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1};
+  return collide_batch_ex(A, B, d_poses, N, d_hit, d_pair_count, d_ws, ws_bytes, stream, &o);
 }
 int distance_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, float* d_min_dist,
                    void* d_ws, size_t ws_bytes, void* stream) {
-  return launch<1, false>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream);
+  return distance_batch_ex(A, B, d_poses, N, d_min_dist, d_ws, ws_bytes, stream, nullptr);
 }
 int distance_batch_stats(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N,
                          float* d_min_dist, void* d_ws, size_t ws_bytes, void* stream) {
-  return launch<1, true>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream);
+  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1};
+  return distance_batch_ex(A, B, d_poses, N, d_min_dist, d_ws, ws_bytes, stream, &o);
 }
 
 int cbvh_check(const void* d_ws, void* stream) {

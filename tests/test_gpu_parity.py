@@ -31,10 +31,10 @@ def M():
     return M
 
 
-def run_collide(M, A, B, poses, stats=False):
+def run_collide(M, A, B, poses, stats=False, descent="larger"):
     P = torch.from_numpy(np.ascontiguousarray(poses)).cuda()
     ws = M.Workspace(A, B, 0)
-    hit, cnt = M.collide_batch(A, B, P, workspace=ws, stats=stats)
+    hit, cnt = M.collide_batch(A, B, P, workspace=ws, stats=stats, descent=descent)
     M.check(ws)
     out = hit.cpu().numpy(), cnt.cpu().numpy().view(np.uint32).astype(np.int64)
     if stats:
@@ -42,10 +42,10 @@ def run_collide(M, A, B, poses, stats=False):
     return out
 
 
-def run_distance(M, A, B, poses, stats=False):
+def run_distance(M, A, B, poses, stats=False, descent="larger"):
     P = torch.from_numpy(np.ascontiguousarray(poses)).cuda()
     ws = M.Workspace(A, B, 1)
-    d = M.distance_batch(A, B, P, workspace=ws, stats=stats)
+    d = M.distance_batch(A, B, P, workspace=ws, stats=stats, descent=descent)
     M.check(ws)
     out = d.cpu().numpy()
     if stats:
@@ -88,6 +88,24 @@ def test_config1_layouts(M, cfg1, Bf, bits):
     A, B = build(M, w.A, Bf, bits), build(M, w.B, Bf, bits)
     hit, gc = run_collide(M, A, B, w.poses)
     check_collide(hit, gc, H, Z, f"cfg1 B={Bf} b={bits}")
+
+
+@pytest.mark.parametrize("Bf", [2, 4, 8])
+def test_config1_alg1_simultaneous_descent(M, cfg1, Bf):
+    # Alg. 1 verbatim (descend both nodes) and the default larger-first rule
+    # reach the same leaf pairs: identical counts on every pose, both in band
+    w, tA, tB, delta, cnt, H, Z = cfg1
+    A, B = build(M, w.A, Bf, 8), build(M, w.B, Bf, 8)
+    h1, c1, s1 = run_collide(M, A, B, w.poses, stats=True, descent="simultaneous")
+    h2, c2, s2 = run_collide(M, A, B, w.poses, stats=True, descent="larger")
+    check_collide(h1, c1, H, Z, f"alg1 B={Bf}")
+    assert np.array_equal(c1, c2) and np.array_equal(h1, h2)
+    assert s1["leaf_pairs"] == s2["leaf_pairs"]  # each (leafA, leafB) pair reached exactly once
+    d1 = run_distance(M, A, B, w.poses[:128], descent="simultaneous")
+    d2 = run_distance(M, A, B, w.poses[:128], descent="larger")
+    d64, _ = O.distance(tA, tB, w.poses[:128])
+    check_distance(d1, d64, delta, "alg1 distance")
+    check_distance(d2, d64, delta, "larger distance")
 
 
 def test_config1_stats_variant_same_answer(M, cfg1):
