@@ -230,6 +230,19 @@ __device__ __forceinline__ Tri to_local(const PoseF& P, const Tri& W) {
   return L;
 }
 
+__device__ __forceinline__ bool tri_boxes_overlap(const Tri& V, const Tri& U) {
+  bool ok = true;
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float vlo = fminf(V.v[0][k], fminf(V.v[1][k], V.v[2][k]));
+    const float vhi = fmaxf(V.v[0][k], fmaxf(V.v[1][k], V.v[2][k]));
+    const float ulo = fminf(U.v[0][k], fminf(U.v[1][k], U.v[2][k]));
+    const float uhi = fmaxf(U.v[0][k], fmaxf(U.v[1][k], U.v[2][k]));
+    ok = ok && !(vhi < ulo || uhi < vlo);
+  }
+  return ok;
+}
+
 // fp64 re-evaluation of a near-contact distance candidate,
 // in the world frame as the distance is defined: A's fp32
 // triangle mapped by the fp32 pose lifted exactly to fp64, B's fp32 triangle
@@ -336,7 +349,9 @@ __device__ __noinline__ unsigned drain_leaves(const Params& p, const WarpCtx c, 
       const Tri TA = load_tri(p.A.tris, ia);
       const Tri TB = to_local(P, load_tri(p.B.tris, ib));
       if (MODE == 0) {
-        hit = tri_tri_overlap(TA, TB);
+        // exact prefilter on the same fp32 coordinates Möller uses: closed
+        // triangles whose AABBs are disjoint cannot intersect
+        hit = tri_boxes_overlap(TA, TB) && tri_tri_overlap(TA, TB);
       } else {
         d = tri_tri_dist(TA, TB);
         // fp32 error here is ~1e-7 x (|t| + model extents); candidates whose
