@@ -243,6 +243,55 @@ __device__ __forceinline__ bool tri_boxes_overlap(const Tri& V, const Tri& U) {
   return ok;
 }
 
+// Conservative box–triangle overlap: the 3 box axes and the triangle normal
+// of the 13-axis separating-axis test (the 9 edge axes are skipped).
+__device__ __forceinline__ bool box_tri_overlap(const float lo[3], const float hi[3], const Tri& T, float eps) {
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float tlo = fminf(T.v[0][k], fminf(T.v[1][k], T.v[2][k]));
+    const float thi = fmaxf(T.v[0][k], fmaxf(T.v[1][k], T.v[2][k]));
+    if (tlo > hi[k] + eps || thi < lo[k] - eps) return false;
+  }
+  float e1[3], e2[3], n[3];
+  vsub(T.v[1], T.v[0], e1);
+  vsub(T.v[2], T.v[0], e2);
+  vcross(e1, e2, n);
+  float sdist = 0.f, rad = 0.f, nrm = 0.f;
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    sdist = fmaf(n[k], 0.5f * (lo[k] + hi[k]) - T.v[0][k], sdist);
+    rad = fmaf(fabsf(n[k]), 0.5f * (hi[k] - lo[k]), rad);
+    nrm += fabsf(n[k]);
+  }
+  return fabsf(sdist) <= fmaf(eps, nrm, rad);
+}
+
+// A's box (A-local) against the triangles of B leaf tb, mapped into A's frame
+__device__ __noinline__ bool box_hits_leaf_local(const PoseF& P, const float lo[3], const float hi[3],
+                                                 const float* trisB, uint32_t tb, float eps) {
+  const uint32_t first = tb & 0x1FFFFFFFu, cnt = ((tb >> 29) & 3u) + 1;
+  for (uint32_t q = 0; q < cnt; ++q)
+    if (box_tri_overlap(lo, hi, to_local(P, load_tri(trisB, first + q)), eps)) return true;
+  return false;
+}
+
+// B's box (world) against the triangles of A leaf ta, mapped into the world
+__device__ __noinline__ bool box_hits_leaf_world(const PoseF& P, const float lo[3], const float hi[3],
+                                                 const float* trisA, uint32_t ta, float eps) {
+  const uint32_t first = ta & 0x1FFFFFFFu, cnt = ((ta >> 29) & 3u) + 1;
+  for (uint32_t q = 0; q < cnt; ++q) {
+    const Tri L = load_tri(trisA, first + q);
+    Tri W;
+    #pragma unroll
+    for (int v = 0; v < 3; ++v)
+      #pragma unroll
+      for (int k = 0; k < 3; ++k)
+        W.v[v][k] = fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], P.t[k])));
+    if (box_tri_overlap(lo, hi, W, eps)) return true;
+  }
+  return false;
+}
+
 // fp64 re-evaluation of a near-contact distance candidate,
 // in the world frame as the distance is defined: A's fp32
 // triangle mapped by the fp32 pose lifted exactly to fp64, B's fp32 triangle
@@ -574,6 +623,12 @@ __global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_cons
         to_float_box(p.B, CB, blo, bhi);
         if (MODE == 0) {
           surv = sat_gap<false>(P, alo, ahi, blo, bhi, eps, nullptr) <= 0.f;
+          // Against a leaf, "intersect" is refined to the leaf's triangles
+          // themselves (still conservative): the partner's box must touch at
+          // least one of them.  B's leaves are ~10x A's in config 5, so the
+          // box alone lets every A leaf crossing a B leaf box through.
+          if (surv && !b_int && (tb & kLeafBit)) surv = box_hits_leaf_local(P, alo, ahi, p.B.tris, tb, eps);
+          else if (surv && !a_int && (ta & kLeafBit)) surv = box_hits_leaf_world(P, blo, bhi, p.A.tris, ta, eps);
         } else {
           sat_gap<true>(P, alo, ahi, blo, bhi, eps, &lb);
           surv = lb < best;
