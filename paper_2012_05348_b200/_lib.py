@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcbvh.so")
+LIB_PATH = os.environ.get("CBVH_LIB") or os.path.join(HERE, "libcbvh.so")
 
 CBVH_OK, CBVH_EINVAL, CBVH_EMESH, CBVH_EBLOB = 0, -1, -2, -3
 CBVH_ECUDA, CBVH_ENOMEM, CBVH_EWORKSPACE, CBVH_EOVERFLOW = -4, -5, -6, -7

@@ -69,6 +69,9 @@ struct Control {
 };
 static_assert(sizeof(Control) == 128, "control block layout");
 
+#ifndef CBVH_MIN_BLOCKS
+#define CBVH_MIN_BLOCKS 1
+#endif
 constexpr int kWarps = 4;           // warps per CTA
 constexpr int kStack = 64;          // smem stack entries per warp
 constexpr int kFields = 16;         // words per stack entry
@@ -471,7 +474,7 @@ __device__ __noinline__ int2 spill_in(const WarpCtx c, int spill_top) {
 }
 
 template <int MODE, bool STATS>
-__global__ void __launch_bounds__(kWarps * 32) traverse_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint32_t smem[];
   const int wib = threadIdx.x >> 5;
   WarpCtx c;
