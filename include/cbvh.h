@@ -92,7 +92,7 @@ typedef struct {
 typedef struct {
   cbvh_header h;
   uint64_t bvh_bytes;      /* topo + codes + treelet table: the compressed hierarchy */
-  uint64_t tri_bytes;      /* leaf-ordered fp32 triangle soup (36 B / triangle) */
+  uint64_t tri_bytes;      /* leaf-ordered fp32 triangle soup (48 B / triangle: 9 floats + 3 pads) */
   double bytes_per_node;   /* bvh_bytes / num_nodes */
   double code_bytes_per_node; /* the BV descriptor alone: 6 * code_width / 8 */
 } cbvh_info;
@@ -172,7 +172,7 @@ typedef struct {
   uint64_t tri_tests;       /* triangle-pair tests */
   uint64_t nodes_decoded;   /* child boxes decoded (records fetched) */
   uint64_t record_bytes;    /* compressed bytes of those records (4 B topo + 6w/8 B codes each) */
-  uint64_t tri_bytes;       /* algorithmic triangle bytes: (c_A + c_B) x 36 B per leaf pair */
+  uint64_t tri_bytes;       /* algorithmic triangle bytes: 36 B x triangles loaded (box-leaf filters + leaf phase) */
   uint64_t spills;          /* stack spill events */
 } cbvh_stats;
 

@@ -330,7 +330,7 @@ struct BlobView {
 template <class X> X rd(const uint8_t* p, size_t off) { X x; std::memcpy(&x, p + off, sizeof(X)); return x; }
 
 bool parse_blob(const uint8_t* p, size_t bytes, BlobView* b) {
-  if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0 || rd<uint32_t>(p, 4) != 1) return false;
+  if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0 || rd<uint32_t>(p, 4) != 2) return false;
   b->p = p; b->bytes = bytes;
   b->B = rd<uint32_t>(p, 8); b->bits = rd<uint32_t>(p, 12); b->T = rd<uint32_t>(p, 16);
   b->c = rd<uint32_t>(p, 20); b->w = rd<uint32_t>(p, 24); b->n_nodes = rd<uint32_t>(p, 28);
@@ -835,7 +835,9 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
         // soup must equal the mesh triangle, vertex by vertex
         for (int v = 0; v < 3; ++v)
           for (int a = 0; a < 3; ++a)
-            if (soup[9ull * s + 3 * v + a] != verts[3 * tris[3 * ti + v] + a]) report[4]++;
+            if (soup[12ull * s + 3 * v + a] != verts[3 * tris[3 * ti + v] + a]) report[4]++;
+        for (int z = 9; z < 12; ++z)
+          if (soup[12ull * s + z] != 0.0f) report[4]++;
         subtree_tris[n].push_back(ti);
       }
     } else {

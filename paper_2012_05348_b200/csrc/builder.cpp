@@ -241,7 +241,7 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   std::vector<uint32_t> topo(n), tri_index;
   std::vector<float> soup;
   tri_index.reserve(nt);
-  soup.reserve(9 * (size_t)nt);
+  soup.reserve(12 * (size_t)nt);
   int depth = 0, leaves = 0;
   for (int nid = 0; nid < n; ++nid) {
     const BNode& nd = bd.nodes[order[nid]];
@@ -252,8 +252,10 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
       for (int k = nd.tri_begin; k < nd.tri_end; ++k) {
         int t = bd.perm[k];
         tri_index.push_back((uint32_t)t);
+        // 48-byte record: v0 v1 v2 (xyz fp32) + 3 zero pads, three 16-B vectors
         for (int v = 0; v < 3; ++v)
           for (int a = 0; a < 3; ++a) soup.push_back(mesh->vertices[3 * (int64_t)mesh->triangles[3 * (int64_t)t + v] + a]);
+        for (int z = 0; z < 3; ++z) soup.push_back(0.0f);
       }
       topo[nid] = 0x80000000u | ((cnt - 1) << 29) | first;
     } else {
@@ -271,7 +273,7 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   size_t off_codes = align256(off_topo + 4 * (size_t)n);
   size_t off_treelets = align256(off_codes + code_bytes_node * (size_t)n);
   size_t off_tris = align256(off_treelets + 32 * treelets.size());
-  size_t off_tri_index = align256(off_tris + 36 * (size_t)nt);
+  size_t off_tri_index = align256(off_tris + 48 * (size_t)nt);
   size_t total = align256(off_tri_index + 4 * (size_t)nt);
   try {
     out.assign(total, 0);
@@ -279,7 +281,7 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
     return set_error(CBVH_ENOMEM, "blob allocation failed");
   }
   std::memcpy(&out[0], "CBVH", 4);
-  put<uint32_t>(out, 4, 1u);
+  put<uint32_t>(out, 4, 2u);
   put<uint32_t>(out, 8, (uint32_t)branching);
   put<uint32_t>(out, 12, (uint32_t)bits);
   put<uint32_t>(out, 16, (uint32_t)T);
@@ -319,7 +321,7 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
     put<uint32_t>(out, o + 24, (uint32_t)treelets[k].first);
     put<uint32_t>(out, o + 28, (uint32_t)treelets[k].count);
   }
-  std::memcpy(&out[off_tris], soup.data(), 36 * (size_t)nt);
+  std::memcpy(&out[off_tris], soup.data(), 48 * (size_t)nt);
   std::memcpy(&out[off_tri_index], tri_index.data(), 4 * (size_t)nt);
   return CBVH_OK;
 }
@@ -329,7 +331,7 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
   if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0) return set_error(CBVH_EBLOB, "bad magic");
   auto u32 = [&](size_t o) { uint32_t x; std::memcpy(&x, p + o, 4); return x; };
   auto u64 = [&](size_t o) { uint64_t x; std::memcpy(&x, p + o, 8); return x; };
-  if (u32(4) != 1) return set_error(CBVH_EBLOB, "unsupported blob version");
+  if (u32(4) != 2) return set_error(CBVH_EBLOB, "unsupported blob version");
   h->branching = u32(8); h->bits = u32(12); h->treelet_nodes = u32(16); h->leaf_size = u32(20);
   h->code_width = u32(24); h->num_nodes = u32(28); h->num_tris = u32(32); h->num_treelets = u32(36);
   h->depth = u32(40); h->num_leaves = u32(44);
@@ -348,7 +350,7 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
   if (h->off_topo < 256 || h->off_topo + 4ull * h->num_nodes > h->off_codes ||
       h->off_codes + cb * h->num_nodes > h->off_treelets ||
       h->off_treelets + 32ull * h->num_treelets > h->off_tris ||
-      h->off_tris + 36ull * h->num_tris > h->off_tri_index ||
+      h->off_tris + 48ull * h->num_tris > h->off_tri_index ||
       h->off_tri_index + 4ull * h->num_tris > h->total_bytes)
     return set_error(CBVH_EBLOB, "bad section offsets");
   if ((h->off_topo | h->off_codes | h->off_tris) & 15) return set_error(CBVH_EBLOB, "misaligned sections");
@@ -389,7 +391,7 @@ int cbvh_blob_info(const uint8_t* h_blob, size_t bytes, cbvh_info* out) {
   if (rc) return rc;
   const cbvh_header& h = out->h;
   out->bvh_bytes = 4ull * h.num_nodes + (6ull * h.code_width / 8) * h.num_nodes + 32ull * h.num_treelets;
-  out->tri_bytes = 36ull * h.num_tris;
+  out->tri_bytes = 48ull * h.num_tris;
   out->bytes_per_node = (double)out->bvh_bytes / (double)h.num_nodes;
   out->code_bytes_per_node = 6.0 * h.code_width / 8.0;
   return CBVH_OK;

@@ -211,11 +211,14 @@ __device__ __forceinline__ float sat_gap(const PoseF& P, const float alo[3], con
 using Tri = TriT<float>;
 using Tri64 = TriT<double>;
 
+// 48-byte triangle records: three 16-byte vector loads
 __device__ __forceinline__ Tri load_tri(const float* tris, uint32_t i) {
-  const float* p = tris + 9ull * i;
+  const float4* p = reinterpret_cast<const float4*>(tris + 12ull * i);
+  const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
   Tri T;
-  #pragma unroll
-  for (int k = 0; k < 9; ++k) T.v[k / 3][k % 3] = __ldg(p + k);
+  T.v[0][0] = a.x; T.v[0][1] = a.y; T.v[0][2] = a.z;
+  T.v[1][0] = a.w; T.v[1][1] = b.x; T.v[1][2] = b.y;
+  T.v[2][0] = b.z; T.v[2][1] = b.w; T.v[2][2] = c.x;
   return T;
 }
 
@@ -269,19 +272,22 @@ __device__ __forceinline__ bool box_tri_overlap(const float lo[3], const float h
   return fabsf(sdist) <= fmaf(eps, nrm, rad);
 }
 
-// A's box (A-local) against the triangles of B leaf tb, mapped into A's frame
-__device__ __noinline__ bool box_hits_leaf_local(const PoseF& P, const float lo[3], const float hi[3],
-                                                 const float* trisB, uint32_t tb, float eps) {
+// A's box (A-local) against the triangles of B leaf tb, mapped into A's
+// frame: bit q of the result = triangle q of the leaf may touch the box
+__device__ __noinline__ uint32_t box_hits_leaf_local(const PoseF& P, const float lo[3], const float hi[3],
+                                                     const float* trisB, uint32_t tb, float eps) {
   const uint32_t first = tb & 0x1FFFFFFFu, cnt = ((tb >> 29) & 3u) + 1;
+  uint32_t m = 0;
   for (uint32_t q = 0; q < cnt; ++q)
-    if (box_tri_overlap(lo, hi, to_local(P, load_tri(trisB, first + q)), eps)) return true;
-  return false;
+    if (box_tri_overlap(lo, hi, to_local(P, load_tri(trisB, first + q)), eps)) m |= 1u << q;
+  return m;
 }
 
 // B's box (world) against the triangles of A leaf ta, mapped into the world
-__device__ __noinline__ bool box_hits_leaf_world(const PoseF& P, const float lo[3], const float hi[3],
-                                                 const float* trisA, uint32_t ta, float eps) {
+__device__ __noinline__ uint32_t box_hits_leaf_world(const PoseF& P, const float lo[3], const float hi[3],
+                                                     const float* trisA, uint32_t ta, float eps) {
   const uint32_t first = ta & 0x1FFFFFFFu, cnt = ((ta >> 29) & 3u) + 1;
+  uint32_t m = 0;
   for (uint32_t q = 0; q < cnt; ++q) {
     const Tri L = load_tri(trisA, first + q);
     Tri W;
@@ -290,9 +296,9 @@ __device__ __noinline__ bool box_hits_leaf_world(const PoseF& P, const float lo[
       #pragma unroll
       for (int k = 0; k < 3; ++k)
         W.v[v][k] = fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], P.t[k])));
-    if (box_tri_overlap(lo, hi, W, eps)) return true;
+    if (box_tri_overlap(lo, hi, W, eps)) m |= 1u << q;
   }
-  return false;
+  return m;
 }
 
 // fp64 re-evaluation of a near-contact distance candidate,
@@ -304,17 +310,16 @@ __device__ __noinline__ bool box_hits_leaf_world(const PoseF& P, const float lo[
 __device__ __noinline__ float tri_dist_fp64(const PoseF& P, const float* trisA, uint32_t ia,
                                             const float* trisB, uint32_t ib) {
   Tri64 a, b;
+  const Tri TA = load_tri(trisA, ia), TB = load_tri(trisB, ib);
   #pragma unroll
   for (int v = 0; v < 3; ++v) {
-    const double x0 = (double)__ldg(trisA + 9ull * ia + 3 * v);
-    const double x1 = (double)__ldg(trisA + 9ull * ia + 3 * v + 1);
-    const double x2 = (double)__ldg(trisA + 9ull * ia + 3 * v + 2);
     #pragma unroll
-    for (int k = 0; k < 3; ++k)
-      a.v[v][k] = fma((double)P.R[k][0], x0, fma((double)P.R[k][1], x1, fma((double)P.R[k][2], x2, (double)P.t[k])));
+    for (int k = 0; k < 3; ++k) {
+      a.v[v][k] = fma((double)P.R[k][0], (double)TA.v[v][0],
+                      fma((double)P.R[k][1], (double)TA.v[v][1], fma((double)P.R[k][2], (double)TA.v[v][2], (double)P.t[k])));
+      b.v[v][k] = (double)TB.v[v][k];
+    }
   }
-  #pragma unroll
-  for (int k = 0; k < 9; ++k) b.v[k / 3][k % 3] = (double)__ldg(trisB + 9ull * ib + k);
   return (float)tri_tri_dist(a, b);
 }
 
@@ -322,7 +327,7 @@ __device__ __noinline__ float tri_dist_fp64(const PoseF& P, const float* trisA, 
 // the traversal kernel
 // ----------------------------------------------------------------------------
 
-constexpr int kWarpSmemWords = kFields * kStack + 3 * kLeafQ;
+constexpr int kWarpSmemWords = kFields * kStack + 4 * kLeafQ;
 
 // child pairs of an item: Alg. 1 enumerates children of every side it
 // descends (flags chosen at push time, see descent_flags)
@@ -345,14 +350,13 @@ __device__ __forceinline__ uint32_t descent_flags(int rule, uint32_t ta, uint32_
   return ea >= eb ? kDescA : kDescB;
 }
 
-__device__ __forceinline__ int tri_pair_count(uint32_t ta, uint32_t tb) {
-  return (int)(((ta >> 29) & 3u) + 1) * (int)(((tb >> 29) & 3u) + 1);
-}
+// all triangles of a leaf: low (ntri) bits set
+__device__ __forceinline__ uint32_t full_mask(uint32_t t) { return (2u << ((t >> 29) & 3u)) - 1u; }
 
 // per-warp constant context (registers); mutable counters live in the kernel
 struct WarpCtx {
   uint32_t* st;     // stack SoA [kFields][kStack]
-  uint32_t* lq;     // leaf queue SoA [3][kLeafQ]: pose, topoA, topoB
+  uint32_t* lq;     // leaf queue SoA [4][kLeafQ]: pose, topoA, topoB, triangle masks (A bits 0-3, B bits 4-7)
   uint32_t* spill;  // this warp's global spill area [kSpillCap][kFields]
   int lane;
 };
@@ -366,13 +370,14 @@ __device__ __noinline__ unsigned drain_leaves(const Params& p, const WarpCtx c, 
   int head = 0;
   while (head < nleaf) {
     int avail = min(32, nleaf - head);
-    uint32_t pose = 0, ta = 0, tb = 0;
+    uint32_t pose = 0, ta = 0, tb = 0, mk = 0;
     int n = 0;
     if (c.lane < avail) {
       pose = c.lq[0 * kLeafQ + head + c.lane];
       ta = c.lq[1 * kLeafQ + head + c.lane];
       tb = c.lq[2 * kLeafQ + head + c.lane];
-      n = tri_pair_count(ta, tb);
+      mk = c.lq[3 * kLeafQ + head + c.lane];
+      n = __popc(mk & 15u) * __popc(mk >> 4);  // only triangles the box filters kept
     }
     int incl = n;
     #pragma unroll
@@ -389,11 +394,13 @@ __device__ __noinline__ unsigned drain_leaves(const Params& p, const WarpCtx c, 
     const uint32_t my_pose = __shfl_sync(FULL, pose, e);
     const uint32_t my_ta = __shfl_sync(FULL, ta, e);
     const uint32_t my_tb = __shfl_sync(FULL, tb, e);
+    const uint32_t my_mk = __shfl_sync(FULL, mk, e);
     const bool valid = c.lane < total;
     const int k = c.lane - start_e;
-    const int nb = (int)((my_tb >> 29) & 3u) + 1;
-    const uint32_t ia = (my_ta & 0x1FFFFFFFu) + (uint32_t)(k / nb);
-    const uint32_t ib = (my_tb & 0x1FFFFFFFu) + (uint32_t)(k % nb);
+    const uint32_t mA = my_mk & 15u, mB = my_mk >> 4;
+    const int nb = max(1, __popc(mB));
+    const uint32_t ia = (my_ta & 0x1FFFFFFFu) + (uint32_t)__fns(mA, 0, k / nb + 1);
+    const uint32_t ib = (my_tb & 0x1FFFFFFFu) + (uint32_t)__fns(mB, 0, k % nb + 1);
     bool hit = false;
     float d = FLT_MAX;
     if (valid) {
@@ -507,6 +514,7 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
             c.lq[0 * kLeafQ + slot] = base + c.lane;
             c.lq[1 * kLeafQ + slot] = p.A.root_topo;
             c.lq[2 * kLeafQ + slot] = p.B.root_topo;
+            c.lq[3 * kLeafQ + slot] = full_mask(p.A.root_topo) | (full_mask(p.B.root_topo) << 4);
           } else {
             const int slot = top + c.lane;
             c.st[F_POSE * kStack + slot] =
@@ -600,6 +608,7 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
       uint32_t cta = ta, ctb = tb;
       bool surv = false;
       float lb = 0.f;
+      uint32_t mskA = 15u, mskB = 15u;
       if (valid) {
         if (a_int) {
           const uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
@@ -629,9 +638,22 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
           // Against a leaf, "intersect" is refined to the leaf's triangles
           // themselves (still conservative): the partner's box must touch at
           // least one of them.  B's leaves are ~10x A's in config 5, so the
-          // box alone lets every A leaf crossing a B leaf box through.
-          if (surv && !b_int && (tb & kLeafBit)) surv = box_hits_leaf_local(P, alo, ahi, p.B.tris, tb, eps);
-          else if (surv && !a_int && (ta & kLeafBit)) surv = box_hits_leaf_world(P, blo, bhi, p.A.tris, ta, eps);
+          // box alone lets every A leaf crossing a B leaf box through.  For a
+          // leaf pair both sides are filtered and the surviving triangles are
+          // recorded as masks for the leaf phase.
+          // (a leaf whose box is smaller than its partner's is not filtered:
+          // its few small triangles would rarely reject the larger box)
+          const float ext_a = (ahi[0] - alo[0]) + (ahi[1] - alo[1]) + (ahi[2] - alo[2]);
+          const float ext_b = (bhi[0] - blo[0]) + (bhi[1] - blo[1]) + (bhi[2] - blo[2]);
+          const bool la = (cta & kLeafBit) != 0, lb2 = (ctb & kLeafBit) != 0;
+          if (surv && lb2 && (la || ext_b >= ext_a)) {
+            mskB = box_hits_leaf_local(P, alo, ahi, p.B.tris, ctb, eps);
+            surv = mskB != 0u;
+          }
+          if (surv && la && (lb2 || ext_a >= ext_b)) {
+            mskA = box_hits_leaf_world(P, blo, bhi, p.A.tris, cta, eps);
+            surv = mskA != 0u;
+          }
         } else {
           sat_gap<true>(P, alo, ahi, blo, bhi, eps, &lb);
           surv = lb < best;
@@ -684,6 +706,7 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
           c.lq[0 * kLeafQ + s2] = pose;
           c.lq[1 * kLeafQ + s2] = cta;
           c.lq[2 * kLeafQ + s2] = ctb;
+          c.lq[3 * kLeafQ + s2] = (mskA & full_mask(cta)) | ((mskB & full_mask(ctb)) << 4);
         }
         nleaf += __popc(lm);
         if (STATS) {

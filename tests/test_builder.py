@@ -114,7 +114,7 @@ def test_bytes_per_node_accounting(cfg1):
         i = M.build_compressed_bvh(A.vertices, A.triangles, 4, bits, 32).info
         assert i["code_bytes_per_node"] == cw  # 6 corrections x field width
         assert i["bvh_bytes"] == (4 + cw) * i["num_nodes"] + 32 * i["num_treelets"]
-        assert i["tri_bytes"] == 36 * A.num_triangles
+        assert i["tri_bytes"] == 48 * A.num_triangles
         assert i["code_bytes_per_node"] <= 0.25 * 24 or bits == 16  # S:344 (b=8: 6 B vs 24 B fp32)
 
 
