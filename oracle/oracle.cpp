@@ -836,8 +836,17 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
         for (int v = 0; v < 3; ++v)
           for (int a = 0; a < 3; ++a)
             if (soup[12ull * s + 3 * v + a] != verts[3 * tris[3 * ti + v] + a]) report[4]++;
-        for (int z = 9; z < 12; ++z)
-          if (soup[12ull * s + z] != 0.0f) report[4]++;
+        // stored normal: the fp64 cross product of the edges, rounded to fp32
+        {
+          double V[3][3];
+          for (int v = 0; v < 3; ++v)
+            for (int a = 0; a < 3; ++a) V[v][a] = (double)verts[3 * tris[3 * ti + v] + a];
+          double e1[3], e2[3], nn[3];
+          sub(V[1], V[0], e1); sub(V[2], V[0], e2); cross(e1, e2, nn);
+          double mag = std::sqrt(dot(nn, nn));
+          for (int a = 0; a < 3; ++a)
+            if (std::fabs((double)soup[12ull * s + 9 + a] - nn[a]) > 1e-6 * mag) report[4]++;
+        }
         subtree_tris[n].push_back(ti);
       }
     } else {

@@ -252,10 +252,21 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
       for (int k = nd.tri_begin; k < nd.tri_end; ++k) {
         int t = bd.perm[k];
         tri_index.push_back((uint32_t)t);
-        // 48-byte record: v0 v1 v2 (xyz fp32) + 3 zero pads, three 16-B vectors
+        // 48-byte record: v0 v1 v2 (xyz fp32) and n = (v1 - v0) x (v2 - v0)
+        // (computed in fp64 from the fp32 vertices, rounded once) — three
+        // 16-byte vectors; the normal serves the box-vs-triangle filters
+        double w[3][3];
         for (int v = 0; v < 3; ++v)
-          for (int a = 0; a < 3; ++a) soup.push_back(mesh->vertices[3 * (int64_t)mesh->triangles[3 * (int64_t)t + v] + a]);
-        for (int z = 0; z < 3; ++z) soup.push_back(0.0f);
+          for (int a = 0; a < 3; ++a) {
+            float x = mesh->vertices[3 * (int64_t)mesh->triangles[3 * (int64_t)t + v] + a];
+            soup.push_back(x);
+            w[v][a] = (double)x;
+          }
+        double e1[3] = {w[1][0] - w[0][0], w[1][1] - w[0][1], w[1][2] - w[0][2]};
+        double e2[3] = {w[2][0] - w[0][0], w[2][1] - w[0][1], w[2][2] - w[0][2]};
+        soup.push_back((float)(e1[1] * e2[2] - e1[2] * e2[1]));
+        soup.push_back((float)(e1[2] * e2[0] - e1[0] * e2[2]));
+        soup.push_back((float)(e1[0] * e2[1] - e1[1] * e2[0]));
       }
       topo[nid] = 0x80000000u | ((cnt - 1) << 29) | first;
     } else {

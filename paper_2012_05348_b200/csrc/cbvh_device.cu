@@ -249,56 +249,79 @@ __device__ __forceinline__ bool tri_boxes_overlap(const Tri& V, const Tri& U) {
   return ok;
 }
 
-// Conservative box–triangle overlap: the 3 box axes and the triangle normal
-// of the 13-axis separating-axis test (the 9 edge axes are skipped).
-__device__ __forceinline__ bool box_tri_overlap(const float lo[3], const float hi[3], const Tri& T, float eps) {
+// Conservative box–triangle overlap for the leaf filters: the partner box is
+// an oriented box (center c, half extents h along the columns of M) in the
+// triangles' own frame, so the triangles are used as stored, with their
+// precomputed normals.  Tested axes: the 3 frame axes (AABB of the triangle
+// vs the box's AABB) and the triangle normal (a subset of the 13-axis SAT,
+// so never a false rejection; eps covers fp32 rounding).
+// DIR 0: A's box (A-local) vs B's triangles (world):   M = R,   c = R ca + t
+// DIR 1: B's box (world)   vs A's triangles (A-local): M = R^T, c = R^T (cb - t)
+// Bit q of the result: triangle q of the leaf may touch the box.
+template <int DIR>
+__device__ __noinline__ uint32_t obb_hits_leaf(const PoseF& P, const float lo[3], const float hi[3],
+                                               const float* tris, uint32_t leaf, float eps) {
+  float M[3][3];
   #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const float tlo = fminf(T.v[0][k], fminf(T.v[1][k], T.v[2][k]));
-    const float thi = fmaxf(T.v[0][k], fmaxf(T.v[1][k], T.v[2][k]));
-    if (tlo > hi[k] + eps || thi < lo[k] - eps) return false;
-  }
-  float e1[3], e2[3], n[3];
-  vsub(T.v[1], T.v[0], e1);
-  vsub(T.v[2], T.v[0], e2);
-  vcross(e1, e2, n);
-  float sdist = 0.f, rad = 0.f, nrm = 0.f;
-  #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    sdist = fmaf(n[k], 0.5f * (lo[k] + hi[k]) - T.v[0][k], sdist);
-    rad = fmaf(fabsf(n[k]), 0.5f * (hi[k] - lo[k]), rad);
-    nrm += fabsf(n[k]);
-  }
-  return fabsf(sdist) <= fmaf(eps, nrm, rad);
-}
-
-// A's box (A-local) against the triangles of B leaf tb, mapped into A's
-// frame: bit q of the result = triangle q of the leaf may touch the box
-__device__ __noinline__ uint32_t box_hits_leaf_local(const PoseF& P, const float lo[3], const float hi[3],
-                                                     const float* trisB, uint32_t tb, float eps) {
-  const uint32_t first = tb & 0x1FFFFFFFu, cnt = ((tb >> 29) & 3u) + 1;
-  uint32_t m = 0;
-  for (uint32_t q = 0; q < cnt; ++q)
-    if (box_tri_overlap(lo, hi, to_local(P, load_tri(trisB, first + q)), eps)) m |= 1u << q;
-  return m;
-}
-
-// B's box (world) against the triangles of A leaf ta, mapped into the world
-__device__ __noinline__ uint32_t box_hits_leaf_world(const PoseF& P, const float lo[3], const float hi[3],
-                                                     const float* trisA, uint32_t ta, float eps) {
-  const uint32_t first = ta & 0x1FFFFFFFu, cnt = ((ta >> 29) & 3u) + 1;
-  uint32_t m = 0;
-  for (uint32_t q = 0; q < cnt; ++q) {
-    const Tri L = load_tri(trisA, first + q);
-    Tri W;
+  for (int r = 0; r < 3; ++r)
     #pragma unroll
-    for (int v = 0; v < 3; ++v)
-      #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        W.v[v][k] = fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], P.t[k])));
-    if (box_tri_overlap(lo, hi, W, eps)) m |= 1u << q;
+    for (int q = 0; q < 3; ++q) M[r][q] = DIR == 0 ? P.R[r][q] : P.R[q][r];
+  float h[3], c[3], rad[3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) h[k] = 0.5f * (hi[k] - lo[k]);
+  {
+    float m[3];
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) m[k] = 0.5f * (lo[k] + hi[k]) - (DIR == 0 ? 0.f : P.t[k]);
+    #pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      c[r] = fmaf(M[r][0], m[0], fmaf(M[r][1], m[1], M[r][2] * m[2])) + (DIR == 0 ? P.t[r] : 0.f);
+      rad[r] = fmaf(fabsf(M[r][0]), h[0], fmaf(fabsf(M[r][1]), h[1], fabsf(M[r][2]) * h[2])) + eps;
+    }
   }
-  return m;
+  const uint32_t first = leaf & 0x1FFFFFFFu, cnt = ((leaf >> 29) & 3u) + 1;
+  float4 rec[4][3];
+  #pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q < (int)cnt) {
+      const float4* p4 = reinterpret_cast<const float4*>(tris + 12ull * (first + q));
+      rec[q][0] = __ldg(p4); rec[q][1] = __ldg(p4 + 1); rec[q][2] = __ldg(p4 + 2);
+    }
+  }
+  uint32_t mask = 0;
+  #pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q >= (int)cnt) break;
+    const float v0[3] = {rec[q][0].x, rec[q][0].y, rec[q][0].z};
+    const float v1[3] = {rec[q][0].w, rec[q][1].x, rec[q][1].y};
+    const float v2[3] = {rec[q][1].z, rec[q][1].w, rec[q][2].x};
+    const float n[3] = {rec[q][2].y, rec[q][2].z, rec[q][2].w};
+    bool ok = true;
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float tlo = fminf(v0[k], fminf(v1[k], v2[k]));
+      const float thi = fmaxf(v0[k], fmaxf(v1[k], v2[k]));
+      ok = ok && !(tlo > c[k] + rad[k] || thi < c[k] - rad[k]);
+    }
+    // normal axis: |n.(c - v0)| <= sum_m |n.M_m| h_m  (+ slack)
+    const float sdist = fmaf(n[0], c[0] - v0[0], fmaf(n[1], c[1] - v0[1], n[2] * (c[2] - v0[2])));
+    float r = 0.f;
+    #pragma unroll
+    for (int m = 0; m < 3; ++m) r = fmaf(fabsf(fmaf(n[0], M[0][m], fmaf(n[1], M[1][m], n[2] * M[2][m]))), h[m], r);
+    const float nrm = fabsf(n[0]) + fabsf(n[1]) + fabsf(n[2]);
+    ok = ok && fabsf(sdist) <= fmaf(eps, nrm, r);
+    if (ok) mask |= 1u << q;
+  }
+  return mask;
+}
+
+// packed list of the set bits of a <= 4-bit mask: 2-bit indices, count
+__device__ __forceinline__ uint32_t pack_list(uint32_t m) {
+  uint32_t list = 0, n = 0;
+  #pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (m & (1u << q)) { list |= (uint32_t)q << (2 * n); ++n; }
+  return list | (n << 8);
 }
 
 // fp64 re-evaluation of a near-contact distance candidate,
@@ -377,7 +400,7 @@ __device__ __noinline__ unsigned drain_leaves(const Params& p, const WarpCtx c, 
       ta = c.lq[1 * kLeafQ + head + c.lane];
       tb = c.lq[2 * kLeafQ + head + c.lane];
       mk = c.lq[3 * kLeafQ + head + c.lane];
-      n = __popc(mk & 15u) * __popc(mk >> 4);  // only triangles the box filters kept
+      n = (int)((mk >> 8) & 7u) * (int)((mk >> 19) & 7u);  // only triangles the box filters kept
     }
     int incl = n;
     #pragma unroll
@@ -397,10 +420,11 @@ __device__ __noinline__ unsigned drain_leaves(const Params& p, const WarpCtx c, 
     const uint32_t my_mk = __shfl_sync(FULL, mk, e);
     const bool valid = c.lane < total;
     const int k = c.lane - start_e;
-    const uint32_t mA = my_mk & 15u, mB = my_mk >> 4;
-    const int nb = max(1, __popc(mB));
-    const uint32_t ia = (my_ta & 0x1FFFFFFFu) + (uint32_t)__fns(mA, 0, k / nb + 1);
-    const uint32_t ib = (my_tb & 0x1FFFFFFFu) + (uint32_t)__fns(mB, 0, k % nb + 1);
+    // my_mk: bits 0-7 / 11-18 packed 2-bit triangle lists of A / B, counts at 8 / 19
+    const int nb = max(1, (int)((my_mk >> 19) & 7u));
+    const int ka = k / nb, kb = k - ka * nb;
+    const uint32_t ia = (my_ta & 0x1FFFFFFFu) + ((my_mk >> (2 * ka)) & 3u);
+    const uint32_t ib = (my_tb & 0x1FFFFFFFu) + ((my_mk >> (11 + 2 * kb)) & 3u);
     bool hit = false;
     float d = FLT_MAX;
     if (valid) {
@@ -514,7 +538,7 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
             c.lq[0 * kLeafQ + slot] = base + c.lane;
             c.lq[1 * kLeafQ + slot] = p.A.root_topo;
             c.lq[2 * kLeafQ + slot] = p.B.root_topo;
-            c.lq[3 * kLeafQ + slot] = full_mask(p.A.root_topo) | (full_mask(p.B.root_topo) << 4);
+            c.lq[3 * kLeafQ + slot] = pack_list(full_mask(p.A.root_topo)) | (pack_list(full_mask(p.B.root_topo)) << 11);
           } else {
             const int slot = top + c.lane;
             c.st[F_POSE * kStack + slot] =
@@ -647,11 +671,11 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
           const float ext_b = (bhi[0] - blo[0]) + (bhi[1] - blo[1]) + (bhi[2] - blo[2]);
           const bool la = (cta & kLeafBit) != 0, lb2 = (ctb & kLeafBit) != 0;
           if (surv && lb2 && (la || ext_b >= ext_a)) {
-            mskB = box_hits_leaf_local(P, alo, ahi, p.B.tris, ctb, eps);
+            mskB = obb_hits_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps);
             surv = mskB != 0u;
           }
           if (surv && la && (lb2 || ext_a >= ext_b)) {
-            mskA = box_hits_leaf_world(P, blo, bhi, p.A.tris, cta, eps);
+            mskA = obb_hits_leaf<1>(P, blo, bhi, p.A.tris, cta, eps);
             surv = mskA != 0u;
           }
         } else {
@@ -706,7 +730,7 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
           c.lq[0 * kLeafQ + s2] = pose;
           c.lq[1 * kLeafQ + s2] = cta;
           c.lq[2 * kLeafQ + s2] = ctb;
-          c.lq[3 * kLeafQ + s2] = (mskA & full_mask(cta)) | ((mskB & full_mask(ctb)) << 4);
+          c.lq[3 * kLeafQ + s2] = pack_list(mskA & full_mask(cta)) | (pack_list(mskB & full_mask(ctb)) << 11);
         }
         nleaf += __popc(lm);
         if (STATS) {
