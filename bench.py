@@ -242,6 +242,13 @@ def run(args):
     value = N * args.steps * world / T
     hits = int(hit.sum().item())
 
+    if args.quick:
+        if rank == 0:
+            print(json.dumps({"quick": True, "value": value, "ms_per_step": 1e3 * T / args.steps,
+                              "kernel_ms": statistics.mean(kern_ms), "hit_fraction": hits / N,
+                              "lib": os.environ.get("CBVH_LIB", "default")}), flush=True)
+        return
+
     # ---- stats run (untimed): BV-pair tests and algorithmic bytes per launch
     M.collide_batch(A, B, poses, hit, cnt, ws, stats=True)
     st = M.read_stats(ws)
@@ -327,6 +334,7 @@ def main():
     ap.add_argument("--poses", type=int, default=None, help="override the config's pose count")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
+    ap.add_argument("--quick", action="store_true", help="timed steps only (A/B comparisons)")
     ap.add_argument("--cpu-poses", type=int, default=100000)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-poses", type=int, default=2048, help="poses per --impl reference step")

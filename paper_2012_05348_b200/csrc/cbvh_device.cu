@@ -64,7 +64,8 @@ struct DevTree {
 struct Control {
   unsigned int error;
   unsigned int cursor;
-  unsigned int pad[14];
+  unsigned int pad[6];
+  unsigned long long t_start, t_exhausted, t_end, t_pad;  // globaltimer (stats variant)
   unsigned long long stats[8];
 };
 static_assert(sizeof(Control) == 128, "control block layout");
@@ -101,6 +102,12 @@ constexpr uint32_t kDescA = 0x40000000u;
 constexpr uint32_t kDescB = 0x80000000u;
 
 constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -249,70 +256,90 @@ __device__ __forceinline__ bool tri_boxes_overlap(const Tri& V, const Tri& U) {
   return ok;
 }
 
-// Conservative box–triangle overlap for the leaf filters: the partner box is
-// an oriented box (center c, half extents h along the columns of M) in the
-// triangles' own frame, so the triangles are used as stored, with their
-// precomputed normals.  Tested axes: the 3 frame axes (AABB of the triangle
-// vs the box's AABB) and the triangle normal (a subset of the 13-axis SAT,
-// so never a false rejection; eps covers fp32 rounding).
-// DIR 0: A's box (A-local) vs B's triangles (world):   M = R,   c = R ca + t
-// DIR 1: B's box (world)   vs A's triangles (A-local): M = R^T, c = R^T (cb - t)
-// Bit q of the result: triangle q of the leaf may touch the box.
-template <int DIR>
-__device__ __noinline__ uint32_t obb_hits_leaf(const PoseF& P, const float lo[3], const float hi[3],
-                                               const float* tris, uint32_t leaf, float eps) {
-  float M[3][3];
+// Conservative box–triangle overlap (separating-axis test, Akenine-Möller's
+// triangle–box formulation): the 3 box axes, the triangle normal and, with
+// CBVH_TRIBOX_EDGES, the 9 edge x box-axis crosses.  Testing fewer axes
+// only makes the filter looser, never wrong; eps covers fp32 rounding.
+#ifndef CBVH_TRIBOX_EDGES
+#define CBVH_TRIBOX_EDGES 0
+#endif
+__device__ __forceinline__ bool box_tri_overlap(const float c[3], const float h[3], const Tri& T, float eps) {
+  float v[3][3];
   #pragma unroll
-  for (int r = 0; r < 3; ++r)
+  for (int q = 0; q < 3; ++q)
     #pragma unroll
-    for (int q = 0; q < 3; ++q) M[r][q] = DIR == 0 ? P.R[r][q] : P.R[q][r];
-  float h[3], c[3], rad[3];
+    for (int k = 0; k < 3; ++k) v[q][k] = T.v[q][k] - c[k];  // box-centred
   #pragma unroll
-  for (int k = 0; k < 3; ++k) h[k] = 0.5f * (hi[k] - lo[k]);
-  {
-    float m[3];
-    #pragma unroll
-    for (int k = 0; k < 3; ++k) m[k] = 0.5f * (lo[k] + hi[k]) - (DIR == 0 ? 0.f : P.t[k]);
-    #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      c[r] = fmaf(M[r][0], m[0], fmaf(M[r][1], m[1], M[r][2] * m[2])) + (DIR == 0 ? P.t[r] : 0.f);
-      rad[r] = fmaf(fabsf(M[r][0]), h[0], fmaf(fabsf(M[r][1]), h[1], fabsf(M[r][2]) * h[2])) + eps;
-    }
+  for (int k = 0; k < 3; ++k) {
+    const float tlo = fminf(v[0][k], fminf(v[1][k], v[2][k]));
+    const float thi = fmaxf(v[0][k], fmaxf(v[1][k], v[2][k]));
+    if (tlo > h[k] + eps || thi < -h[k] - eps) return false;
   }
-  const uint32_t first = leaf & 0x1FFFFFFFu, cnt = ((leaf >> 29) & 3u) + 1;
-  float4 rec[4][3];
+  float e[3][3];
+  vsub(v[1], v[0], e[0]);
+  vsub(v[2], v[1], e[1]);
+  vsub(v[0], v[2], e[2]);
+  float n[3];
+  vcross(e[0], e[1], n);
+  const float nrm = fabsf(n[0]) + fabsf(n[1]) + fabsf(n[2]);
+  const float rad_n = fmaf(fabsf(n[0]), h[0], fmaf(fabsf(n[1]), h[1], fabsf(n[2]) * h[2]));
+  if (fabsf(vdot(n, v[0])) > fmaf(eps, nrm, rad_n)) return false;
+#if CBVH_TRIBOX_EDGES
   #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (q < (int)cnt) {
-      const float4* p4 = reinterpret_cast<const float4*>(tris + 12ull * (first + q));
-      rec[q][0] = __ldg(p4); rec[q][1] = __ldg(p4 + 1); rec[q][2] = __ldg(p4 + 2);
-    }
-  }
-  uint32_t mask = 0;
-  #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (q >= (int)cnt) break;
-    const float v0[3] = {rec[q][0].x, rec[q][0].y, rec[q][0].z};
-    const float v1[3] = {rec[q][0].w, rec[q][1].x, rec[q][1].y};
-    const float v2[3] = {rec[q][1].z, rec[q][1].w, rec[q][2].x};
-    const float n[3] = {rec[q][2].y, rec[q][2].z, rec[q][2].w};
-    bool ok = true;
+  for (int i = 0; i < 3; ++i) {
+    // axis a = e_i x unit_k: only two components are non-zero
     #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const float tlo = fminf(v0[k], fminf(v1[k], v2[k]));
-      const float thi = fmaxf(v0[k], fmaxf(v1[k], v2[k]));
-      ok = ok && !(tlo > c[k] + rad[k] || thi < c[k] - rad[k]);
+      const int k1 = (k + 1) % 3, k2 = (k + 2) % 3;
+      // a = e_i x u_k  ->  a[k1] = e[i][k2], a[k2] = -e[i][k1]
+      const float a1 = e[i][k2], a2 = -e[i][k1];
+      const float p0 = a1 * v[0][k1] + a2 * v[0][k2];
+      const float p1 = a1 * v[1][k1] + a2 * v[1][k2];
+      const float p2 = a1 * v[2][k1] + a2 * v[2][k2];
+      const float r = fabsf(a1) * h[k1] + fabsf(a2) * h[k2];
+      const float sl = eps * (fabsf(a1) + fabsf(a2));
+      if (fminf(p0, fminf(p1, p2)) > r + sl || fmaxf(p0, fmaxf(p1, p2)) < -r - sl) return false;
     }
-    // normal axis: |n.(c - v0)| <= sum_m |n.M_m| h_m  (+ slack)
-    const float sdist = fmaf(n[0], c[0] - v0[0], fmaf(n[1], c[1] - v0[1], n[2] * (c[2] - v0[2])));
-    float r = 0.f;
-    #pragma unroll
-    for (int m = 0; m < 3; ++m) r = fmaf(fabsf(fmaf(n[0], M[0][m], fmaf(n[1], M[1][m], n[2] * M[2][m]))), h[m], r);
-    const float nrm = fabsf(n[0]) + fabsf(n[1]) + fabsf(n[2]);
-    ok = ok && fabsf(sdist) <= fmaf(eps, nrm, r);
-    if (ok) mask |= 1u << q;
   }
-  return mask;
+#endif
+  return true;
+}
+
+// A's box (A-local) against the triangles of B leaf tb, mapped into A's
+// frame: bit q of the result = triangle q of the leaf may touch the box
+__device__ __noinline__ uint32_t box_hits_leaf_local(const PoseF& P, const float lo[3], const float hi[3],
+                                                     const float* trisB, uint32_t tb, float eps) {
+  const uint32_t first = tb & 0x1FFFFFFFu, cnt = ((tb >> 29) & 3u) + 1;
+  float c[3], h[3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
+  uint32_t m = 0;
+  #pragma unroll 1
+  for (uint32_t q = 0; q < cnt; ++q)
+    if (box_tri_overlap(c, h, to_local(P, load_tri(trisB, first + q)), eps)) m |= 1u << q;
+  return m;
+}
+
+// B's box (world) against the triangles of A leaf ta, mapped into the world
+__device__ __noinline__ uint32_t box_hits_leaf_world(const PoseF& P, const float lo[3], const float hi[3],
+                                                     const float* trisA, uint32_t ta, float eps) {
+  const uint32_t first = ta & 0x1FFFFFFFu, cnt = ((ta >> 29) & 3u) + 1;
+  float c[3], h[3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
+  uint32_t m = 0;
+  #pragma unroll 1
+  for (uint32_t q = 0; q < cnt; ++q) {
+    const Tri L = load_tri(trisA, first + q);
+    Tri W;
+    #pragma unroll
+    for (int v = 0; v < 3; ++v)
+      #pragma unroll
+      for (int k = 0; k < 3; ++k)
+        W.v[v][k] = fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], P.t[k])));
+    if (box_tri_overlap(c, h, W, eps)) m |= 1u << q;
+  }
+  return m;
 }
 
 // packed list of the set bits of a <= 4-bit mask: 2-bit indices, count
@@ -519,6 +546,7 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
   const unsigned lt = lanemask_lt();
   const float scale_ab = p.A.maxabs + p.B.maxabs;
   const bool root_leafpair = (p.A.root_topo & kLeafBit) && (p.B.root_topo & kLeafBit);
+  if (STATS && c.lane == 0) atomicMin(&p.ctl->t_start, globaltimer_ns());
 
   while (true) {
     // ---- acquire poses when the stack runs low: push their root pairs
@@ -530,6 +558,7 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
       base = __shfl_sync(FULL, base, 0);
       if (base >= (unsigned)p.N) {
         poses_left = false;
+        if (STATS && c.lane == 0) atomicMin(&p.ctl->t_exhausted, globaltimer_ns());
       } else {
         const int k = min(kGrab, p.N - (int)base);
         if (c.lane < k) {
@@ -665,17 +694,12 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
           // box alone lets every A leaf crossing a B leaf box through.  For a
           // leaf pair both sides are filtered and the surviving triangles are
           // recorded as masks for the leaf phase.
-          // (a leaf whose box is smaller than its partner's is not filtered:
-          // its few small triangles would rarely reject the larger box)
-          const float ext_a = (ahi[0] - alo[0]) + (ahi[1] - alo[1]) + (ahi[2] - alo[2]);
-          const float ext_b = (bhi[0] - blo[0]) + (bhi[1] - blo[1]) + (bhi[2] - blo[2]);
-          const bool la = (cta & kLeafBit) != 0, lb2 = (ctb & kLeafBit) != 0;
-          if (surv && lb2 && (la || ext_b >= ext_a)) {
-            mskB = obb_hits_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps);
+          if (surv && (ctb & kLeafBit)) {
+            mskB = box_hits_leaf_local(P, alo, ahi, p.B.tris, ctb, eps);
             surv = mskB != 0u;
           }
-          if (surv && la && (lb2 || ext_a >= ext_b)) {
-            mskA = obb_hits_leaf<1>(P, blo, bhi, p.A.tris, cta, eps);
+          if (surv && (cta & kLeafBit)) {
+            mskA = box_hits_leaf_world(P, blo, bhi, p.A.tris, cta, eps);
             surv = mskA != 0u;
           }
         } else {
@@ -752,6 +776,7 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
     }
   }
   if (nleaf > 0) s_tri += drain_leaves<MODE>(p, c, nleaf);
+  if (STATS && c.lane == 0) atomicMax(&p.ctl->t_end, globaltimer_ns());
   if (STATS) {
     unsigned long long d = s_dec, r = s_rec, lb = s_lbytes;
     #pragma unroll
@@ -784,8 +809,12 @@ __global__ void init_kernel(Params p, int reset_stats) {
   if (i == 0) {
     p.ctl->cursor = 0u;
     p.ctl->error = 0u;
-    if (reset_stats)
+    if (reset_stats) {
       for (int s = 0; s < 8; ++s) p.ctl->stats[s] = 0ull;
+      p.ctl->t_start = ~0ull;
+      p.ctl->t_exhausted = ~0ull;
+      p.ctl->t_end = 0ull;
+    }
   }
 }
 
