@@ -174,6 +174,8 @@ typedef struct {
   uint64_t record_bytes;    /* compressed bytes of those records (4 B topo + 6w/8 B codes each) */
   uint64_t tri_bytes;       /* algorithmic triangle bytes: 36 B x triangles loaded (box-leaf filters + leaf phase) */
   uint64_t spills;          /* stack spill events */
+  uint64_t kernel_ns;       /* traversal kernel span (first warp start .. last warp end), globaltimer */
+  uint64_t tail_ns;         /* span from pose-cursor exhaustion to the last warp's end (load-imbalance tail) */
 } cbvh_stats;
 
 /* Same as collide_batch / distance_batch but also accumulate cbvh_stats in

@@ -1051,13 +1051,16 @@ int cbvh_check(const void* d_ws, void* stream) {
 int cbvh_read_stats(const void* d_ws, cbvh_stats* out, void* stream) {
   if (!d_ws || !out) return set_error(CBVH_EINVAL, "null argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  unsigned long long v[8];
-  cudaError_t e = cudaMemcpyAsync(v, static_cast<const uint8_t*>(d_ws) + offsetof(Control, stats), sizeof v,
-                                  cudaMemcpyDeviceToHost, st);
+  Control ctl;
+  cudaError_t e = cudaMemcpyAsync(&ctl, d_ws, sizeof ctl, cudaMemcpyDeviceToHost, st);
+  const unsigned long long* v = ctl.stats;
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "cbvh_read_stats");
   out->bv_tests = v[0]; out->expansions = v[1]; out->leaf_pairs = v[2]; out->tri_tests = v[3];
   out->nodes_decoded = v[4]; out->record_bytes = v[5]; out->tri_bytes = v[6]; out->spills = v[7];
+  const bool timed = ctl.t_end > 0 && ctl.t_start != ~0ull && ctl.t_end >= ctl.t_start;
+  out->kernel_ns = timed ? ctl.t_end - ctl.t_start : 0;
+  out->tail_ns = (timed && ctl.t_exhausted != ~0ull && ctl.t_end >= ctl.t_exhausted) ? ctl.t_end - ctl.t_exhausted : 0;
   return CBVH_OK;
 }
 
