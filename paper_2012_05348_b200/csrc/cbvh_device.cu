@@ -305,38 +305,61 @@ __device__ __forceinline__ bool box_tri_overlap(const float c[3], const float h[
   return true;
 }
 
-// A's box (A-local) against the triangles of B leaf tb, mapped into A's
-// frame: bit q of the result = triangle q of the leaf may touch the box
-__device__ __noinline__ uint32_t box_hits_leaf_local(const PoseF& P, const float lo[3], const float hi[3],
-                                                     const float* trisB, uint32_t tb, float eps) {
-  const uint32_t first = tb & 0x1FFFFFFFu, cnt = ((tb >> 29) & 3u) + 1;
-  float c[3], h[3];
-  #pragma unroll
-  for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
-  uint32_t m = 0;
-  #pragma unroll 1
-  for (uint32_t q = 0; q < cnt; ++q)
-    if (box_tri_overlap(c, h, to_local(P, load_tri(trisB, first + q)), eps)) m |= 1u << q;
-  return m;
+// Triangle q of a leaf as three 16-byte vectors.
+struct TriRec {
+  float4 a, b, c;
+};
+__device__ __forceinline__ TriRec load_rec(const float* tris, uint32_t i) {
+  const float4* p = reinterpret_cast<const float4*>(tris + 12ull * i);
+  return TriRec{__ldg(p), __ldg(p + 1), __ldg(p + 2)};
+}
+__device__ __forceinline__ Tri rec_tri(const TriRec& r) {
+  Tri T;
+  T.v[0][0] = r.a.x; T.v[0][1] = r.a.y; T.v[0][2] = r.a.z;
+  T.v[1][0] = r.a.w; T.v[1][1] = r.b.x; T.v[1][2] = r.b.y;
+  T.v[2][0] = r.b.z; T.v[2][1] = r.b.w; T.v[2][2] = r.c.x;
+  return T;
 }
 
-// B's box (world) against the triangles of A leaf ta, mapped into the world
-__device__ __noinline__ uint32_t box_hits_leaf_world(const PoseF& P, const float lo[3], const float hi[3],
-                                                     const float* trisA, uint32_t ta, float eps) {
-  const uint32_t first = ta & 0x1FFFFFFFu, cnt = ((ta >> 29) & 3u) + 1;
+#ifndef CBVH_FILTER_PIPE
+#define CBVH_FILTER_PIPE 1
+#endif
+
+// The box (centre c, half extents h) against the triangles of a leaf, each
+// mapped into the box's frame (DIR 0: B's world triangles into A's frame by
+// R^T (v - t); DIR 1: A's local triangles into the world by R v + t).  Bit q
+// of the result: triangle q of the leaf may touch the box.  The next
+// triangle's record is fetched while the current one is tested.
+template <int DIR>
+__device__ __noinline__ uint32_t box_hits_leaf(const PoseF& P, const float lo[3], const float hi[3],
+                                               const float* tris, uint32_t leaf, float eps) {
+  const uint32_t first = leaf & 0x1FFFFFFFu, cnt = ((leaf >> 29) & 3u) + 1;
   float c[3], h[3];
   #pragma unroll
   for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
   uint32_t m = 0;
+#if CBVH_FILTER_PIPE == 1
+  TriRec next = load_rec(tris, first);
   #pragma unroll 1
   for (uint32_t q = 0; q < cnt; ++q) {
-    const Tri L = load_tri(trisA, first + q);
+    const TriRec cur = next;
+    if (q + 1 < cnt) next = load_rec(tris, first + q + 1);
+    const Tri L = rec_tri(cur);
+#else
+  #pragma unroll 1
+  for (uint32_t q = 0; q < cnt; ++q) {
+    const Tri L = rec_tri(load_rec(tris, first + q));
+#endif
     Tri W;
-    #pragma unroll
-    for (int v = 0; v < 3; ++v)
+    if (DIR == 0) {
+      W = to_local(P, L);
+    } else {
       #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        W.v[v][k] = fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], P.t[k])));
+      for (int v = 0; v < 3; ++v)
+        #pragma unroll
+        for (int k = 0; k < 3; ++k)
+          W.v[v][k] = fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], P.t[k])));
+    }
     if (box_tri_overlap(c, h, W, eps)) m |= 1u << q;
   }
   return m;
@@ -695,11 +718,11 @@ __global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(
           // leaf pair both sides are filtered and the surviving triangles are
           // recorded as masks for the leaf phase.
           if (surv && (ctb & kLeafBit)) {
-            mskB = box_hits_leaf_local(P, alo, ahi, p.B.tris, ctb, eps);
+            mskB = box_hits_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps);
             surv = mskB != 0u;
           }
           if (surv && (cta & kLeafBit)) {
-            mskA = box_hits_leaf_world(P, blo, bhi, p.A.tris, cta, eps);
+            mskA = box_hits_leaf<1>(P, blo, bhi, p.A.tris, cta, eps);
             surv = mskA != 0u;
           }
         } else {
