@@ -71,7 +71,7 @@ struct Control {
 static_assert(sizeof(Control) == 128, "control block layout");
 
 #ifndef CBVH_MIN_BLOCKS
-#define CBVH_MIN_BLOCKS 1
+#define CBVH_MIN_BLOCKS 4
 #endif
 constexpr int kWarps = 4;           // warps per CTA
 constexpr int kStack = 64;          // smem stack entries per warp
@@ -330,8 +330,16 @@ __device__ __forceinline__ Tri rec_tri(const TriRec& r) {
 // R^T (v - t); DIR 1: A's local triangles into the world by R v + t).  Bit q
 // of the result: triangle q of the leaf may touch the box.  The next
 // triangle's record is fetched while the current one is tested.
+#ifndef CBVH_FILTER_INLINE
+#define CBVH_FILTER_INLINE 1
+#endif
+#if CBVH_FILTER_INLINE
+#define CBVH_FILTER_ATTR __forceinline__
+#else
+#define CBVH_FILTER_ATTR __noinline__
+#endif
 template <int DIR>
-__device__ __noinline__ uint32_t box_hits_leaf(const PoseF& P, const float lo[3], const float hi[3],
+__device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float lo[3], const float hi[3],
                                                const float* tris, uint32_t leaf, float eps) {
   const uint32_t first = leaf & 0x1FFFFFFFu, cnt = ((leaf >> 29) & 3u) + 1;
   float c[3], h[3];
@@ -555,7 +563,7 @@ __device__ __noinline__ int2 spill_in(const WarpCtx c, int spill_top) {
 }
 
 template <int MODE, bool STATS>
-__global__ void __launch_bounds__(kWarps * 32, CBVH_MIN_BLOCKS) traverse_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) traverse_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint32_t smem[];
   const int wib = threadIdx.x >> 5;
   WarpCtx c;
