@@ -63,9 +63,12 @@ struct DevTree {
 
 struct Control {
   unsigned int error;
-  unsigned int cursor;
-  unsigned int pad[6];
-  unsigned long long t_start, t_exhausted, t_end, t_pad;  // globaltimer (stats variant)
+  unsigned int cursor;   // next pose to acquire
+  unsigned int busy;     // warps holding work (termination of the stealing phase)
+  unsigned int lock;     // donation-queue lock
+  unsigned int q_top;    // items in the donation queue
+  unsigned int pad[3];
+  unsigned long long t_start, t_exhausted, t_end, steals;  // globaltimer (stats variant), items stolen
   unsigned long long stats[8];
 };
 static_assert(sizeof(Control) == 128, "control block layout");
@@ -78,6 +81,8 @@ constexpr int kStack = 64;          // smem stack entries per warp
 constexpr int kFields = 16;         // words per stack entry
 constexpr int kLeafQ = 64;          // leaf-queue entries per warp
 constexpr int kSpillCap = 2048;     // global spill entries per warp
+constexpr int kQueueCap = 16384;    // donation-queue items (work stealing)
+constexpr int kDonate = 16;         // max items donated / taken at once
 constexpr int kGrab = 8;            // poses acquired per cursor atomic
 constexpr int kLowWater = 4;        // acquire poses when the stack is below this
 
@@ -93,6 +98,8 @@ struct Params {
   uint32_t* dist_bits;   // float bits of the running minimum distance
   Control* ctl;
   uint32_t* spill;       // [num_warps][kSpillCap][kFields]
+  uint32_t* queue;       // donation queue [kQueueCap][kFields]
+  int nwarps;            // warps in the grid
   int descent;           // CBVH_DESCENT_SIMULTANEOUS (Alg. 1 verbatim) or CBVH_DESCENT_LARGER
 };
 
@@ -562,6 +569,87 @@ __device__ __noinline__ int2 spill_in(const WarpCtx c, int spill_top) {
   return make_int2(n, base);
 }
 
+// ---------------------------------------------------------------- work stealing
+// A global LIFO of donated items guarded by a warp-level lock.  Busy warps in
+// the stealing phase (poses exhausted) donate the bottom of their stacks —
+// the shallowest, largest sub-traversals — when warps are idle; idle warps
+// take them.  Termination: nobody busy and the queue empty, checked under the
+// lock (takers increment `busy` under the lock, donors are busy while
+// donating), so no work can appear afterwards.  Queue data bypasses L1.
+
+__device__ __forceinline__ unsigned ld_volatile(const unsigned* p) {
+  return *reinterpret_cast<const volatile unsigned*>(p);
+}
+
+__device__ __forceinline__ void q_lock(Control* ctl, int lane) {
+  if (lane == 0)
+    while (atomicCAS(&ctl->lock, 0u, 1u) != 0u) __nanosleep(64);
+  __syncwarp();
+  __threadfence();
+}
+
+__device__ __forceinline__ void q_unlock(Control* ctl, int lane) {
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) atomicExch(&ctl->lock, 0u);
+}
+
+// Move up to kDonate items from the bottom of the smem stack to the queue;
+// returns the new top.
+__device__ __noinline__ int donate(const Params& p, const WarpCtx c, int top) {
+  q_lock(p.ctl, c.lane);
+  const unsigned qn = ld_volatile(&p.ctl->q_top);
+  int k = min(top / 2, kDonate);
+  k = min(k, kQueueCap - (int)qn);
+  if (k > 0) {
+    for (int idx = c.lane; idx < k * kFields; idx += 32) {
+      const int e = idx / kFields, f = idx % kFields;
+      __stcg(&p.queue[(size_t)(qn + e) * kFields + f], c.st[f * kStack + e]);
+    }
+    __threadfence();
+    __syncwarp();
+    if (c.lane == 0) atomicExch(&p.ctl->q_top, qn + (unsigned)k);
+  }
+  q_unlock(p.ctl, c.lane);
+  if (k <= 0) return top;
+  const int rest = top - k;
+  for (int idx = c.lane; idx < rest * kFields; idx += 32) {
+    const int e = idx % rest, f = idx / rest;
+    const uint32_t v = c.st[f * kStack + e + k];
+    __syncwarp(__activemask());
+    c.st[f * kStack + e] = v;
+  }
+  __syncwarp();
+  return rest;
+}
+
+// Take up to kDonate items into the (empty) smem stack.  Returns the number
+// taken, or -1 when the whole traversal is finished.
+__device__ __noinline__ int steal(const Params& p, const WarpCtx c) {
+  const unsigned qn0 = ld_volatile(&p.ctl->q_top);
+  if (qn0 == 0u && ld_volatile(&p.ctl->busy) != 0u) return 0;
+  q_lock(p.ctl, c.lane);
+  const unsigned qn = ld_volatile(&p.ctl->q_top);
+  int k = 0;
+  if (qn > 0u) {
+    k = min((int)qn, kDonate);
+    const unsigned base = qn - (unsigned)k;
+    for (int idx = c.lane; idx < k * kFields; idx += 32) {
+      const int e = idx / kFields, f = idx % kFields;
+      c.st[f * kStack + e] = __ldcg(&p.queue[(size_t)(base + e) * kFields + f]);
+    }
+    if (c.lane == 0) {
+      atomicExch(&p.ctl->q_top, base);
+      atomicAdd(&p.ctl->busy, 1u);
+    }
+  } else if (ld_volatile(&p.ctl->busy) == 0u) {
+    k = -1;
+  }
+  q_unlock(p.ctl, c.lane);
+  __syncwarp();
+  return k;
+}
+
 template <int MODE, bool STATS>
 __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) traverse_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint32_t smem[];
@@ -572,6 +660,9 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
   c.lq = c.st + kFields * kStack;
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * kFields;
   int top = 0, nleaf = 0, spill_top = 0;
+  bool idle = false;
+  unsigned donate_tick = 0;
+  unsigned long long s_steal = 0;
   unsigned long long s_bv = 0, s_exp = 0, s_leaf = 0, s_tri = 0, s_dec = 0, s_rec = 0, s_lbytes = 0, s_spill = 0;
   bool poses_left = true;
   const unsigned lt = lanemask_lt();
@@ -629,7 +720,30 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
         continue;
       }
       if (poses_left) continue;
-      break;
+      // ---- out of poses and items: finish the leaf queue, then steal
+      if (nleaf > 0) {
+        s_tri += drain_leaves<MODE>(p, c, nleaf);
+        nleaf = 0;
+      }
+      if (!idle) {
+        if (c.lane == 0) atomicSub(&p.ctl->busy, 1u);
+        idle = true;
+      }
+      const int got = steal(p, c);
+      if (got > 0) {
+        top = got;
+        idle = false;
+        if (STATS) s_steal += got;
+        continue;
+      }
+      if (got < 0) break;  // global termination: nobody busy, queue empty
+      __nanosleep(256);
+      continue;
+    }
+    // ---- donate the bottom of the stack to idle warps (stealing phase only)
+    if (!poses_left && top >= 8 && (++donate_tick & 3) == 0) {
+      const unsigned busy = ld_volatile(&p.ctl->busy), qn = ld_volatile(&p.ctl->q_top);
+      if (busy < (unsigned)p.nwarps && qn < (unsigned)(p.nwarps - busy)) top = donate(p, c, top);
     }
 
     // ---- pop as many items as fill 32 lanes with child pairs
@@ -825,6 +939,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
       atomicAdd(&p.ctl->stats[5], r);
       atomicAdd(&p.ctl->stats[6], lb);
       atomicAdd(&p.ctl->stats[7], s_spill);
+      atomicAdd(&p.ctl->steals, s_steal);
     }
   }
 }
@@ -840,11 +955,15 @@ __global__ void init_kernel(Params p, int reset_stats) {
   if (i == 0) {
     p.ctl->cursor = 0u;
     p.ctl->error = 0u;
+    p.ctl->busy = (unsigned)p.nwarps;
+    p.ctl->lock = 0u;
+    p.ctl->q_top = 0u;
     if (reset_stats) {
       for (int s = 0; s < 8; ++s) p.ctl->stats[s] = 0ull;
       p.ctl->t_start = ~0ull;
       p.ctl->t_exhausted = ~0ull;
       p.ctl->t_end = 0ull;
+      p.ctl->steals = 0ull;
     }
   }
 }
@@ -904,7 +1023,7 @@ static int max_warps(int mode) {
 }
 
 static size_t workspace_for_warps(int warps) {
-  return 256 + (size_t)warps * kSpillCap * kFields * sizeof(uint32_t);
+  return 256 + (size_t)warps * kSpillCap * kFields * sizeof(uint32_t) + (size_t)kQueueCap * kFields * sizeof(uint32_t);
 }
 
 static DevTree make_tree(const cbvh_bvh* T) {
@@ -956,6 +1075,8 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
   p.dist_bits = reinterpret_cast<uint32_t*>(d_dist);
   p.ctl = static_cast<Control*>(d_ws);
   p.spill = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + 256);
+  p.queue = p.spill + (size_t)s.warps * kSpillCap * kFields;
+  p.nwarps = s.warps;
   p.descent = descent;
   int ib = (int)((N + 255) / 256);
   ib = ib < 1 ? 1 : (ib > 4096 ? 4096 : ib);
@@ -1092,6 +1213,7 @@ int cbvh_read_stats(const void* d_ws, cbvh_stats* out, void* stream) {
   const bool timed = ctl.t_end > 0 && ctl.t_start != ~0ull && ctl.t_end >= ctl.t_start;
   out->kernel_ns = timed ? ctl.t_end - ctl.t_start : 0;
   out->tail_ns = (timed && ctl.t_exhausted != ~0ull && ctl.t_end >= ctl.t_exhausted) ? ctl.t_end - ctl.t_exhausted : 0;
+  out->steals = ctl.steals;
   return CBVH_OK;
 }
 
