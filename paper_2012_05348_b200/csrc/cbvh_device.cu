@@ -581,6 +581,14 @@ __device__ __forceinline__ unsigned ld_volatile(const unsigned* p) {
   return *reinterpret_cast<const volatile unsigned*>(p);
 }
 
+// lane 0 reads, the warp agrees (values other warps change must not diverge
+// the warp's control flow)
+__device__ __forceinline__ unsigned ld_uniform(const unsigned* p, int lane) {
+  unsigned v = 0;
+  if (lane == 0) v = ld_volatile(p);
+  return __shfl_sync(FULL, v, 0);
+}
+
 __device__ __forceinline__ void q_lock(Control* ctl, int lane) {
   if (lane == 0)
     while (atomicCAS(&ctl->lock, 0u, 1u) != 0u) __nanosleep(64);
@@ -598,7 +606,7 @@ __device__ __forceinline__ void q_unlock(Control* ctl, int lane) {
 // returns the new top.
 __device__ __noinline__ int donate(const Params& p, const WarpCtx c, int top) {
   q_lock(p.ctl, c.lane);
-  const unsigned qn = ld_volatile(&p.ctl->q_top);
+  const unsigned qn = ld_uniform(&p.ctl->q_top, c.lane);
   int k = min(top / 2, kDonate);
   k = min(k, kQueueCap - (int)qn);
   if (k > 0) {
@@ -626,10 +634,10 @@ __device__ __noinline__ int donate(const Params& p, const WarpCtx c, int top) {
 // Take up to kDonate items into the (empty) smem stack.  Returns the number
 // taken, or -1 when the whole traversal is finished.
 __device__ __noinline__ int steal(const Params& p, const WarpCtx c) {
-  const unsigned qn0 = ld_volatile(&p.ctl->q_top);
-  if (qn0 == 0u && ld_volatile(&p.ctl->busy) != 0u) return 0;
+  const unsigned qn0 = ld_uniform(&p.ctl->q_top, c.lane);
+  if (qn0 == 0u && ld_uniform(&p.ctl->busy, c.lane) != 0u) return 0;
   q_lock(p.ctl, c.lane);
-  const unsigned qn = ld_volatile(&p.ctl->q_top);
+  const unsigned qn = ld_uniform(&p.ctl->q_top, c.lane);
   int k = 0;
   if (qn > 0u) {
     k = min((int)qn, kDonate);
@@ -642,7 +650,7 @@ __device__ __noinline__ int steal(const Params& p, const WarpCtx c) {
       atomicExch(&p.ctl->q_top, base);
       atomicAdd(&p.ctl->busy, 1u);
     }
-  } else if (ld_volatile(&p.ctl->busy) == 0u) {
+  } else if (ld_uniform(&p.ctl->busy, c.lane) == 0u) {
     k = -1;
   }
   q_unlock(p.ctl, c.lane);
@@ -742,7 +750,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
     }
     // ---- donate the bottom of the stack to idle warps (stealing phase only)
     if (!poses_left && top >= 8 && (++donate_tick & 3) == 0) {
-      const unsigned busy = ld_volatile(&p.ctl->busy), qn = ld_volatile(&p.ctl->q_top);
+      const unsigned busy = ld_uniform(&p.ctl->busy, c.lane), qn = ld_uniform(&p.ctl->q_top, c.lane);
       if (busy < (unsigned)p.nwarps && qn < (unsigned)(p.nwarps - busy)) top = donate(p, c, top);
     }
 
