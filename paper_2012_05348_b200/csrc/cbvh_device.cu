@@ -581,11 +581,12 @@ __device__ __forceinline__ unsigned ld_volatile(const unsigned* p) {
   return *reinterpret_cast<const volatile unsigned*>(p);
 }
 
-// lane 0 reads, the warp agrees (values other warps change must not diverge
-// the warp's control flow)
-__device__ __forceinline__ unsigned ld_uniform(const unsigned* p, int lane) {
+// Lane 0 reads the current value at L2 (an atomic, never a stale L1 line)
+// and the warp agrees on it: values other warps change must neither be stale
+// under the lock nor diverge the warp's control flow.
+__device__ __forceinline__ unsigned ld_uniform(unsigned* p, int lane) {
   unsigned v = 0;
-  if (lane == 0) v = ld_volatile(p);
+  if (lane == 0) v = atomicOr(p, 0u);
   return __shfl_sync(FULL, v, 0);
 }
 
@@ -620,14 +621,18 @@ __device__ __noinline__ int donate(const Params& p, const WarpCtx c, int top) {
   }
   q_unlock(p.ctl, c.lane);
   if (k <= 0) return top;
+  // shift the remaining items down by k (overlapping: every round reads
+  // before it writes, and a round only reads slots above those it writes)
   const int rest = top - k;
-  for (int idx = c.lane; idx < rest * kFields; idx += 32) {
-    const int e = idx % rest, f = idx / rest;
-    const uint32_t v = c.st[f * kStack + e + k];
-    __syncwarp(__activemask());
-    c.st[f * kStack + e] = v;
+  for (int b = 0; b < rest * kFields; b += 32) {
+    const int idx = b + c.lane;
+    const bool on = idx < rest * kFields;
+    const int e = on ? idx % rest : 0, f = on ? idx / rest : 0;
+    const uint32_t v = on ? c.st[f * kStack + e + k] : 0u;
+    __syncwarp();
+    if (on) c.st[f * kStack + e] = v;
+    __syncwarp();
   }
-  __syncwarp();
   return rest;
 }
 
