@@ -590,6 +590,14 @@ __device__ __forceinline__ unsigned ld_uniform(unsigned* p, int lane) {
   return __shfl_sync(FULL, v, 0);
 }
 
+// Polling hint: an L2 read without an atomic (may be slightly old; every
+// decision that matters is re-checked under the lock with ld_uniform).
+__device__ __forceinline__ unsigned ld_hint(const unsigned* p, int lane) {
+  unsigned v = 0;
+  if (lane == 0) v = __ldcg(p);
+  return __shfl_sync(FULL, v, 0);
+}
+
 __device__ __forceinline__ void q_lock(Control* ctl, int lane) {
   if (lane == 0)
     while (atomicCAS(&ctl->lock, 0u, 1u) != 0u) __nanosleep(64);
@@ -639,8 +647,8 @@ __device__ __noinline__ int donate(const Params& p, const WarpCtx c, int top) {
 // Take up to kDonate items into the (empty) smem stack.  Returns the number
 // taken, or -1 when the whole traversal is finished.
 __device__ __noinline__ int steal(const Params& p, const WarpCtx c) {
-  const unsigned qn0 = ld_uniform(&p.ctl->q_top, c.lane);
-  if (qn0 == 0u && ld_uniform(&p.ctl->busy, c.lane) != 0u) return 0;
+  const unsigned qn0 = ld_hint(&p.ctl->q_top, c.lane);
+  if (qn0 == 0u && ld_hint(&p.ctl->busy, c.lane) != 0u) return 0;
   q_lock(p.ctl, c.lane);
   const unsigned qn = ld_uniform(&p.ctl->q_top, c.lane);
   int k = 0;
@@ -750,12 +758,12 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
         continue;
       }
       if (got < 0) break;  // global termination: nobody busy, queue empty
-      __nanosleep(256);
+      __nanosleep(1024);
       continue;
     }
     // ---- donate the bottom of the stack to idle warps (stealing phase only)
     if (!poses_left && top >= 8 && (++donate_tick & 3) == 0) {
-      const unsigned busy = ld_uniform(&p.ctl->busy, c.lane), qn = ld_uniform(&p.ctl->q_top, c.lane);
+      const unsigned busy = ld_hint(&p.ctl->busy, c.lane), qn = ld_hint(&p.ctl->q_top, c.lane);
       if (busy < (unsigned)p.nwarps && qn < (unsigned)(p.nwarps - busy)) top = donate(p, c, top);
     }
 
