@@ -598,11 +598,14 @@ __device__ __forceinline__ unsigned ld_hint(const unsigned* p, int lane) {
   return __shfl_sync(FULL, v, 0);
 }
 
-__device__ __forceinline__ void q_lock(Control* ctl, int lane) {
-  if (lane == 0)
-    while (atomicCAS(&ctl->lock, 0u, 1u) != 0u) __nanosleep(64);
-  __syncwarp();
-  __threadfence();
+// one attempt, no spinning: a convoy of thousands of idle warps spinning on
+// one lock word starves the lock holder's own atomics
+__device__ __forceinline__ bool q_trylock(Control* ctl, int lane) {
+  unsigned ok = 0;
+  if (lane == 0) ok = atomicCAS(&ctl->lock, 0u, 1u) == 0u;
+  ok = __shfl_sync(FULL, ok, 0);
+  if (ok) __threadfence();
+  return ok != 0;
 }
 
 __device__ __forceinline__ void q_unlock(Control* ctl, int lane) {
@@ -614,7 +617,7 @@ __device__ __forceinline__ void q_unlock(Control* ctl, int lane) {
 // Move up to kDonate items from the bottom of the smem stack to the queue;
 // returns the new top.
 __device__ __noinline__ int donate(const Params& p, const WarpCtx c, int top) {
-  q_lock(p.ctl, c.lane);
+  if (!q_trylock(p.ctl, c.lane)) return top;
   const unsigned qn = ld_uniform(&p.ctl->q_top, c.lane);
   int k = min(top / 2, kDonate);
   k = min(k, kQueueCap - (int)qn);
@@ -649,7 +652,7 @@ __device__ __noinline__ int donate(const Params& p, const WarpCtx c, int top) {
 __device__ __noinline__ int steal(const Params& p, const WarpCtx c) {
   const unsigned qn0 = ld_hint(&p.ctl->q_top, c.lane);
   if (qn0 == 0u && ld_hint(&p.ctl->busy, c.lane) != 0u) return 0;
-  q_lock(p.ctl, c.lane);
+  if (!q_trylock(p.ctl, c.lane)) return 0;
   const unsigned qn = ld_uniform(&p.ctl->q_top, c.lane);
   int k = 0;
   if (qn > 0u) {
@@ -682,7 +685,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * kFields;
   int top = 0, nleaf = 0, spill_top = 0;
   bool idle = false;
-  unsigned donate_tick = 0;
+  unsigned donate_tick = 0, backoff = 256u;
   unsigned long long s_steal = 0;
   unsigned long long s_bv = 0, s_exp = 0, s_leaf = 0, s_tri = 0, s_dec = 0, s_rec = 0, s_lbytes = 0, s_spill = 0;
   bool poses_left = true;
@@ -754,11 +757,13 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
       if (got > 0) {
         top = got;
         idle = false;
+        backoff = 256u;
         if (STATS) s_steal += got;
         continue;
       }
       if (got < 0) break;  // global termination: nobody busy, queue empty
-      __nanosleep(1024);
+      __nanosleep(backoff);
+      backoff = min(backoff * 2u, 8192u);
       continue;
     }
     // ---- donate the bottom of the stack to idle warps (stealing phase only)
