@@ -176,7 +176,7 @@ typedef struct {
   uint64_t spills;          /* stack spill events */
   uint64_t kernel_ns;       /* traversal kernel span (first warp start .. last warp end), globaltimer */
   uint64_t tail_ns;         /* span from pose-cursor exhaustion to the last warp's end (load-imbalance tail) */
-  uint64_t steals;          /* items taken from the work-stealing queue */
+  uint64_t dumped;          /* items handed to a later load-balancing phase (continuations) */
 } cbvh_stats;
 
 /* Same as collide_batch / distance_batch but also accumulate cbvh_stats in

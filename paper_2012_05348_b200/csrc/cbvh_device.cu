@@ -37,7 +37,9 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/cbvh.h"
@@ -61,17 +63,17 @@ struct DevTree {
   int32_t root[6];   // decoded root lattice box
 };
 
+constexpr int kMaxPhases = 8;
+
 struct Control {
   unsigned int error;
-  unsigned int cursor;   // next pose to acquire
-  unsigned int busy;     // warps holding work (termination of the stealing phase)
-  unsigned int lock;     // donation-queue lock
-  unsigned int q_top;    // items in the donation queue
-  unsigned int pad[3];
-  unsigned long long t_start, t_exhausted, t_end, steals;  // globaltimer (stats variant), items stolen
+  unsigned int pad0;
+  unsigned int cursor[kMaxPhases];  // per phase: next pose (phase 0) / continuation item to acquire
+  unsigned int count[kMaxPhases];   // per phase: items dumped for the next phase
+  unsigned long long t_start, t_exhausted, t_end, dumped;  // globaltimer (stats variant), items dumped
   unsigned long long stats[8];
 };
-static_assert(sizeof(Control) == 128, "control block layout");
+static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte workspace header");
 
 #ifndef CBVH_MIN_BLOCKS
 #define CBVH_MIN_BLOCKS 4
@@ -81,8 +83,8 @@ constexpr int kStack = 64;          // smem stack entries per warp
 constexpr int kFields = 16;         // words per stack entry
 constexpr int kLeafQ = 64;          // leaf-queue entries per warp
 constexpr int kSpillCap = 2048;     // global spill entries per warp
-constexpr int kQueueCap = 16384;    // donation-queue items (work stealing)
-constexpr int kDonate = 16;         // max items donated / taken at once
+constexpr int kContCap = 1 << 19;   // continuation-buffer items (per buffer, two buffers)
+constexpr int kGrabItems = 4;       // continuation items acquired per cursor atomic
 constexpr int kGrab = 8;            // poses acquired per cursor atomic
 constexpr int kLowWater = 4;        // acquire poses when the stack is below this
 
@@ -98,8 +100,10 @@ struct Params {
   uint32_t* dist_bits;   // float bits of the running minimum distance
   Control* ctl;
   uint32_t* spill;       // [num_warps][kSpillCap][kFields]
-  uint32_t* queue;       // donation queue [kQueueCap][kFields]
-  int nwarps;            // warps in the grid
+  uint32_t* cont_in;     // continuation items of the previous phase [kContCap][kFields]
+  uint32_t* cont_out;    // continuation items for the next phase
+  int phase;             // 0: poses; >= 1: the previous phase's continuation items
+  int budget;            // iterations a warp may run after its input is exhausted (< 0: unbounded)
   int descent;           // CBVH_DESCENT_SIMULTANEOUS (Alg. 1 verbatim) or CBVH_DESCENT_LARGER
 };
 
@@ -569,109 +573,43 @@ __device__ __noinline__ int2 spill_in(const WarpCtx c, int spill_top) {
   return make_int2(n, base);
 }
 
-// ---------------------------------------------------------------- work stealing
-// A global LIFO of donated items guarded by a warp-level lock.  Busy warps in
-// the stealing phase (poses exhausted) donate the bottom of their stacks —
-// the shallowest, largest sub-traversals — when warps are idle; idle warps
-// take them.  Termination: nobody busy and the queue empty, checked under the
-// lock (takers increment `busy` under the lock, donors are busy while
-// donating), so no work can appear afterwards.  Queue data bypasses L1.
+// ---------------------------------------------------------------- load balancing
+// Persistent warps acquire input from a global cursor.  Once a warp's input
+// is exhausted it may run `budget` more iterations; then it dumps its whole
+// remaining stack (smem + spill) into the continuation buffer and exits.  The
+// next launch (phase) spreads those items over every warp, so a few heavy
+// sub-traversals no longer leave the GPU idle behind them; the last phase
+// runs unbounded.  Items carry their pose id and results are accumulated with
+// atomics, so any warp may finish any item.
 
-__device__ __forceinline__ unsigned ld_volatile(const unsigned* p) {
-  return *reinterpret_cast<const volatile unsigned*>(p);
-}
-
-// Lane 0 reads the current value at L2 (an atomic, never a stale L1 line)
-// and the warp agrees on it: values other warps change must neither be stale
-// under the lock nor diverge the warp's control flow.
-__device__ __forceinline__ unsigned ld_uniform(unsigned* p, int lane) {
-  unsigned v = 0;
-  if (lane == 0) v = atomicOr(p, 0u);
-  return __shfl_sync(FULL, v, 0);
-}
-
-// Polling hint: an L2 read without an atomic (may be slightly old; every
-// decision that matters is re-checked under the lock with ld_uniform).
-__device__ __forceinline__ unsigned ld_hint(const unsigned* p, int lane) {
-  unsigned v = 0;
-  if (lane == 0) v = __ldcg(p);
-  return __shfl_sync(FULL, v, 0);
-}
-
-// one attempt, no spinning: a convoy of thousands of idle warps spinning on
-// one lock word starves the lock holder's own atomics
-__device__ __forceinline__ bool q_trylock(Control* ctl, int lane) {
-  unsigned ok = 0;
-  if (lane == 0) ok = atomicCAS(&ctl->lock, 0u, 1u) == 0u;
-  ok = __shfl_sync(FULL, ok, 0);
-  if (ok) __threadfence();
-  return ok != 0;
-}
-
-__device__ __forceinline__ void q_unlock(Control* ctl, int lane) {
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) atomicExch(&ctl->lock, 0u);
-}
-
-// Move up to kDonate items from the bottom of the smem stack to the queue;
-// returns the new top.
-__device__ __noinline__ int donate(const Params& p, const WarpCtx c, int top) {
-  if (!q_trylock(p.ctl, c.lane)) return top;
-  const unsigned qn = ld_uniform(&p.ctl->q_top, c.lane);
-  int k = min(top / 2, kDonate);
-  k = min(k, kQueueCap - (int)qn);
-  if (k > 0) {
-    for (int idx = c.lane; idx < k * kFields; idx += 32) {
-      const int e = idx / kFields, f = idx % kFields;
-      __stcg(&p.queue[(size_t)(qn + e) * kFields + f], c.st[f * kStack + e]);
+// Reserve n slots of the continuation buffer (compare-and-swap so a failed
+// reservation never leaves a hole); returns the first slot or -1 when full.
+__device__ __forceinline__ int reserve_cont(unsigned* count, int n, int lane) {
+  int base = -1;
+  if (lane == 0) {
+    unsigned cur = __ldcg(count);
+    while (cur + (unsigned)n <= (unsigned)kContCap) {
+      const unsigned prev = atomicCAS(count, cur, cur + (unsigned)n);
+      if (prev == cur) { base = (int)cur; break; }
+      cur = prev;
     }
-    __threadfence();
-    __syncwarp();
-    if (c.lane == 0) atomicExch(&p.ctl->q_top, qn + (unsigned)k);
   }
-  q_unlock(p.ctl, c.lane);
-  if (k <= 0) return top;
-  // shift the remaining items down by k (overlapping: every round reads
-  // before it writes, and a round only reads slots above those it writes)
-  const int rest = top - k;
-  for (int b = 0; b < rest * kFields; b += 32) {
-    const int idx = b + c.lane;
-    const bool on = idx < rest * kFields;
-    const int e = on ? idx % rest : 0, f = on ? idx / rest : 0;
-    const uint32_t v = on ? c.st[f * kStack + e + k] : 0u;
-    __syncwarp();
-    if (on) c.st[f * kStack + e] = v;
-    __syncwarp();
-  }
-  return rest;
+  return __shfl_sync(FULL, base, 0);
 }
 
-// Take up to kDonate items into the (empty) smem stack.  Returns the number
-// taken, or -1 when the whole traversal is finished.
-__device__ __noinline__ int steal(const Params& p, const WarpCtx c) {
-  const unsigned qn0 = ld_hint(&p.ctl->q_top, c.lane);
-  if (qn0 == 0u && ld_hint(&p.ctl->busy, c.lane) != 0u) return 0;
-  if (!q_trylock(p.ctl, c.lane)) return 0;
-  const unsigned qn = ld_uniform(&p.ctl->q_top, c.lane);
-  int k = 0;
-  if (qn > 0u) {
-    k = min((int)qn, kDonate);
-    const unsigned base = qn - (unsigned)k;
-    for (int idx = c.lane; idx < k * kFields; idx += 32) {
-      const int e = idx / kFields, f = idx % kFields;
-      c.st[f * kStack + e] = __ldcg(&p.queue[(size_t)(base + e) * kFields + f]);
-    }
-    if (c.lane == 0) {
-      atomicExch(&p.ctl->q_top, base);
-      atomicAdd(&p.ctl->busy, 1u);
-    }
-  } else if (ld_uniform(&p.ctl->busy, c.lane) == 0u) {
-    k = -1;
+// Dump the smem stack and the spill area; false if the buffer is full.
+__device__ __noinline__ bool dump_items(const Params& p, const WarpCtx c, int top, int spill_top) {
+  const int n = top + spill_top;
+  const int base = reserve_cont(&p.ctl->count[p.phase], n, c.lane);
+  if (base < 0) return false;
+  uint32_t* out = p.cont_out + (size_t)base * kFields;
+  for (int idx = c.lane; idx < spill_top * kFields; idx += 32) out[idx] = c.spill[idx];
+  out += (size_t)spill_top * kFields;
+  for (int idx = c.lane; idx < top * kFields; idx += 32) {
+    const int e = idx / kFields, f = idx % kFields;
+    out[idx] = c.st[f * kStack + e];
   }
-  q_unlock(p.ctl, c.lane);
-  __syncwarp();
-  return k;
+  return true;
 }
 
 template <int MODE, bool STATS>
@@ -684,9 +622,8 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
   c.lq = c.st + kFields * kStack;
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * kFields;
   int top = 0, nleaf = 0, spill_top = 0;
-  bool idle = false;
-  unsigned donate_tick = 0, backoff = 256u;
-  unsigned long long s_steal = 0;
+  int after = 0;  // iterations since the input ran out
+  unsigned long long s_dump = 0;
   unsigned long long s_bv = 0, s_exp = 0, s_leaf = 0, s_tri = 0, s_dec = 0, s_rec = 0, s_lbytes = 0, s_spill = 0;
   bool poses_left = true;
   const unsigned lt = lanemask_lt();
@@ -699,41 +636,60 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
     // (only when nothing is spilled: spilled items are finished first, which
     // bounds the stack by the deepest single traversal, not the batch size)
     if (poses_left && top < kLowWater && spill_top == 0) {
-      unsigned base = 0;
-      if (c.lane == 0) base = atomicAdd(&p.ctl->cursor, (unsigned)kGrab);
-      base = __shfl_sync(FULL, base, 0);
-      if (base >= (unsigned)p.N) {
-        poses_left = false;
-        if (STATS && c.lane == 0) atomicMin(&p.ctl->t_exhausted, globaltimer_ns());
-      } else {
-        const int k = min(kGrab, p.N - (int)base);
-        if (c.lane < k) {
-          if (root_leafpair) {
-            const int slot = nleaf + c.lane;
-            c.lq[0 * kLeafQ + slot] = base + c.lane;
-            c.lq[1 * kLeafQ + slot] = p.A.root_topo;
-            c.lq[2 * kLeafQ + slot] = p.B.root_topo;
-            c.lq[3 * kLeafQ + slot] = pack_list(full_mask(p.A.root_topo)) | (pack_list(full_mask(p.B.root_topo)) << 11);
-          } else {
-            const int slot = top + c.lane;
-            c.st[F_POSE * kStack + slot] =
-                (base + c.lane) | descent_flags(p.descent, p.A.root_topo, p.B.root_topo, p.A.root, p.B.root,
-                                                p.A.cell, p.B.cell);
-            c.st[F_TA * kStack + slot] = p.A.root_topo;
-            c.st[F_TB * kStack + slot] = p.B.root_topo;
-            #pragma unroll
-            for (int q = 0; q < 6; ++q) {
-              c.st[(F_BA + q) * kStack + slot] = (uint32_t)p.A.root[q];
-              c.st[(F_BB + q) * kStack + slot] = (uint32_t)p.B.root[q];
+      if (p.phase == 0) {
+        unsigned base = 0;
+        if (c.lane == 0) base = atomicAdd(&p.ctl->cursor[0], (unsigned)kGrab);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= (unsigned)p.N) {
+          poses_left = false;
+          if (STATS && c.lane == 0) atomicMin(&p.ctl->t_exhausted, globaltimer_ns());
+        } else {
+          const int k = min(kGrab, p.N - (int)base);
+          if (c.lane < k) {
+            if (root_leafpair) {
+              const int slot = nleaf + c.lane;
+              c.lq[0 * kLeafQ + slot] = base + c.lane;
+              c.lq[1 * kLeafQ + slot] = p.A.root_topo;
+              c.lq[2 * kLeafQ + slot] = p.B.root_topo;
+              c.lq[3 * kLeafQ + slot] = pack_list(full_mask(p.A.root_topo)) | (pack_list(full_mask(p.B.root_topo)) << 11);
+            } else {
+              const int slot = top + c.lane;
+              c.st[F_POSE * kStack + slot] =
+                  (base + c.lane) | descent_flags(p.descent, p.A.root_topo, p.B.root_topo, p.A.root, p.B.root,
+                                                  p.A.cell, p.B.cell);
+              c.st[F_TA * kStack + slot] = p.A.root_topo;
+              c.st[F_TB * kStack + slot] = p.B.root_topo;
+              #pragma unroll
+              for (int q = 0; q < 6; ++q) {
+                c.st[(F_BA + q) * kStack + slot] = (uint32_t)p.A.root[q];
+                c.st[(F_BB + q) * kStack + slot] = (uint32_t)p.B.root[q];
+              }
+              c.st[F_LB * kStack + slot] = 0u;
             }
-            c.st[F_LB * kStack + slot] = 0u;
+          }
+          if (root_leafpair) nleaf += k; else top += k;
+          __syncwarp();
+          if (nleaf > kLeafQ - 32) {
+            s_tri += drain_leaves<MODE>(p, c, nleaf);
+            nleaf = 0;
           }
         }
-        if (root_leafpair) nleaf += k; else top += k;
-        __syncwarp();
-        if (nleaf > kLeafQ - 32) {
-          s_tri += drain_leaves<MODE>(p, c, nleaf);
-          nleaf = 0;
+      } else {
+        // continuation items dumped by the previous phase
+        const unsigned avail = p.ctl->count[p.phase - 1];
+        unsigned base = 0;
+        if (c.lane == 0) base = atomicAdd(&p.ctl->cursor[p.phase], (unsigned)kGrabItems);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= avail) {
+          poses_left = false;
+        } else {
+          const int k = min(kGrabItems, (int)(avail - base));
+          for (int idx = c.lane; idx < k * kFields; idx += 32) {
+            const int e = idx / kFields, f = idx % kFields;
+            c.st[f * kStack + top + e] = p.cont_in[(size_t)(base + e) * kFields + f];
+          }
+          top += k;
+          __syncwarp();
         }
       }
     }
@@ -744,32 +700,21 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
         continue;
       }
       if (poses_left) continue;
-      // ---- out of poses and items: finish the leaf queue, then steal
+      break;
+    }
+    // ---- bounded work after the input ran out: hand the rest to the next phase
+    if (!poses_left && p.budget >= 0 && ++after > p.budget) {
       if (nleaf > 0) {
         s_tri += drain_leaves<MODE>(p, c, nleaf);
         nleaf = 0;
       }
-      if (!idle) {
-        if (c.lane == 0) atomicSub(&p.ctl->busy, 1u);
-        idle = true;
+      if (dump_items(p, c, top, spill_top)) {
+        if (STATS) s_dump += top + spill_top;
+        top = 0;
+        spill_top = 0;
+        break;
       }
-      const int got = steal(p, c);
-      if (got > 0) {
-        top = got;
-        idle = false;
-        backoff = 256u;
-        if (STATS) s_steal += got;
-        continue;
-      }
-      if (got < 0) break;  // global termination: nobody busy, queue empty
-      __nanosleep(backoff);
-      backoff = min(backoff * 2u, 8192u);
-      continue;
-    }
-    // ---- donate the bottom of the stack to idle warps (stealing phase only)
-    if (!poses_left && top >= 8 && (++donate_tick & 3) == 0) {
-      const unsigned busy = ld_hint(&p.ctl->busy, c.lane), qn = ld_hint(&p.ctl->q_top, c.lane);
-      if (busy < (unsigned)p.nwarps && qn < (unsigned)(p.nwarps - busy)) top = donate(p, c, top);
+      after = INT_MIN;  // buffer full: finish here
     }
 
     // ---- pop as many items as fill 32 lanes with child pairs
@@ -965,7 +910,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
       atomicAdd(&p.ctl->stats[5], r);
       atomicAdd(&p.ctl->stats[6], lb);
       atomicAdd(&p.ctl->stats[7], s_spill);
-      atomicAdd(&p.ctl->steals, s_steal);
+      atomicAdd(&p.ctl->dumped, s_dump);
     }
   }
 }
@@ -979,17 +924,17 @@ __global__ void init_kernel(Params p, int reset_stats) {
     else p.dist_bits[k] = 0x7f800000u;  // +inf
   }
   if (i == 0) {
-    p.ctl->cursor = 0u;
     p.ctl->error = 0u;
-    p.ctl->busy = (unsigned)p.nwarps;
-    p.ctl->lock = 0u;
-    p.ctl->q_top = 0u;
+    for (int k = 0; k < kMaxPhases; ++k) {
+      p.ctl->cursor[k] = 0u;
+      p.ctl->count[k] = 0u;
+    }
     if (reset_stats) {
       for (int s = 0; s < 8; ++s) p.ctl->stats[s] = 0ull;
       p.ctl->t_start = ~0ull;
       p.ctl->t_exhausted = ~0ull;
       p.ctl->t_end = 0ull;
-      p.ctl->steals = 0ull;
+      p.ctl->dumped = 0ull;
     }
   }
 }
@@ -1049,7 +994,33 @@ static int max_warps(int mode) {
 }
 
 static size_t workspace_for_warps(int warps) {
-  return 256 + (size_t)warps * kSpillCap * kFields * sizeof(uint32_t) + (size_t)kQueueCap * kFields * sizeof(uint32_t);
+  return 256 + (size_t)warps * kSpillCap * kFields * sizeof(uint32_t) +
+         2 * (size_t)kContCap * kFields * sizeof(uint32_t);
+}
+
+// Phase schedule: budgets of the bounded phases, then one
+// unbounded phase.  CBVH_PHASES="b0,b1,..." overrides (tuning only).
+static int phase_budgets(int* out) {
+  static int n = -1;
+  static int b[kMaxPhases];
+  if (n < 0) {
+    n = 0;
+    const char* env = std::getenv("CBVH_PHASES");
+    if (env && *env) {
+      const char* q = env;
+      while (*q && n < kMaxPhases - 1) {
+        b[n++] = std::atoi(q);
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    } else {
+      b[n++] = 32;
+      b[n++] = 32;
+      b[n++] = 64;
+    }
+  }
+  for (int k = 0; k < n; ++k) out[k] = b[k];
+  return n;
 }
 
 static DevTree make_tree(const cbvh_bvh* T) {
@@ -1101,8 +1072,8 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
   p.dist_bits = reinterpret_cast<uint32_t*>(d_dist);
   p.ctl = static_cast<Control*>(d_ws);
   p.spill = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + 256);
-  p.queue = p.spill + (size_t)s.warps * kSpillCap * kFields;
-  p.nwarps = s.warps;
+  uint32_t* cont0 = p.spill + (size_t)s.warps * kSpillCap * kFields;
+  uint32_t* cont1 = cont0 + (size_t)kContCap * kFields;
   p.descent = descent;
   int ib = (int)((N + 255) / 256);
   ib = ib < 1 ? 1 : (ib > 4096 ? 4096 : ib);
@@ -1111,12 +1082,20 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "init_kernel launch");
   if (N == 0) return CBVH_OK;
+  int budgets[kMaxPhases];
+  const int nb = phase_budgets(budgets);
   if (g_ev_start) cudaEventRecord(g_ev_start, st);
-  traverse_kernel<MODE, STATS><<<s.blocks, kWarps * 32, smem_bytes(), st>>>(p);
-  g_launches++;
+  for (int ph = 0; ph <= nb; ++ph) {
+    p.phase = ph;
+    p.budget = ph < nb ? budgets[ph] : -1;
+    p.cont_in = (ph & 1) ? cont0 : cont1;   // phase ph reads what ph - 1 wrote
+    p.cont_out = (ph & 1) ? cont1 : cont0;
+    traverse_kernel<MODE, STATS><<<s.blocks, kWarps * 32, smem_bytes(), st>>>(p);
+    g_launches++;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "traverse_kernel launch");
+  }
   if (g_ev_stop) cudaEventRecord(g_ev_stop, st);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "traverse_kernel launch");
   return CBVH_OK;
 }
 
@@ -1239,7 +1218,7 @@ int cbvh_read_stats(const void* d_ws, cbvh_stats* out, void* stream) {
   const bool timed = ctl.t_end > 0 && ctl.t_start != ~0ull && ctl.t_end >= ctl.t_start;
   out->kernel_ns = timed ? ctl.t_end - ctl.t_start : 0;
   out->tail_ns = (timed && ctl.t_exhausted != ~0ull && ctl.t_end >= ctl.t_exhausted) ? ctl.t_end - ctl.t_exhausted : 0;
-  out->steals = ctl.steals;
+  out->dumped = ctl.dumped;
   return CBVH_OK;
 }
 

@@ -202,7 +202,7 @@ def test_error_paths_device(M, cfg1):
         M.collide_batch(A, B, Pmis, workspace=ws)
     M.collide_batch(A, B, P, workspace=ws)
     M.check(ws)
-    assert M.last_launch_count() == 2
+    assert M.last_launch_count() >= 2  # init + the load-balancing phases
 
 
 # ------------------------------------------------------------------ full-size configs, sampled
