@@ -243,10 +243,14 @@ def run(args):
     hits = int(hit.sum().item())
 
     if args.quick:
+        M.collide_batch(A, B, poses, hit, cnt, ws, stats=True)
+        st = M.read_stats(ws)
         if rank == 0:
             print(json.dumps({"quick": True, "value": value, "ms_per_step": 1e3 * T / args.steps,
                               "kernel_ms": statistics.mean(kern_ms), "hit_fraction": hits / N,
-                              "lib": os.environ.get("CBVH_LIB", "default")}), flush=True)
+                              "lib": os.environ.get("CBVH_LIB", "default"),
+                              "stats_kernel_ms": st["kernel_ns"] / 1e6, "stats_tail_ms": st["tail_ns"] / 1e6,
+                              "dumped": st["dumped"], "launches": M.last_launch_count()}), flush=True)
         return
 
     # ---- stats run (untimed): BV-pair tests and algorithmic bytes per launch
