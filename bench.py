@@ -250,7 +250,8 @@ def run(args):
                               "kernel_ms": statistics.mean(kern_ms), "hit_fraction": hits / N,
                               "lib": os.environ.get("CBVH_LIB", "default"),
                               "stats_kernel_ms": st["kernel_ns"] / 1e6, "stats_tail_ms": st["tail_ns"] / 1e6,
-                              "dumped": st["dumped"], "launches": M.last_launch_count()}), flush=True)
+                              "dumped": st["dumped"], "launches": M.last_launch_count(),
+                              "timeline_ms": [t / 1e6 for t in st["timeline_ns"]]}), flush=True)
         return
 
     # ---- stats run (untimed): BV-pair tests and algorithmic bytes per launch

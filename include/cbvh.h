@@ -177,6 +177,7 @@ typedef struct {
   uint64_t kernel_ns;       /* traversal kernel span (first warp start .. last warp end), globaltimer */
   uint64_t tail_ns;         /* span from pose-cursor exhaustion to the last warp's end (load-imbalance tail) */
   uint64_t dumped;          /* items handed to a later load-balancing phase (continuations) */
+  uint64_t timeline_ns[8];  /* when the pose cursor passed k/8 of N (ns after the kernel start) */
 } cbvh_stats;
 
 /* Same as collide_batch / distance_batch but also accumulate cbvh_stats in

@@ -169,7 +169,7 @@ def check(workspace: Workspace, stream=None) -> None:
 def read_stats(workspace: Workspace, stream=None) -> dict:
     s = L.cbvh_stats()
     L.check(L.load().cbvh_read_stats(C.c_void_p(workspace.ptr), C.byref(s), C.c_void_p(_stream_ptr(stream))))
-    return {k: int(getattr(s, k)) for k, _ in L.cbvh_stats._fields_}
+    return {k: (list(getattr(s, k)) if k == "timeline_ns" else int(getattr(s, k))) for k, _ in L.cbvh_stats._fields_}
 
 
 def last_launch_count() -> int:

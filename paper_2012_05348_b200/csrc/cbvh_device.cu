@@ -72,6 +72,7 @@ struct Control {
   unsigned int count[kMaxPhases];   // per phase: items dumped for the next phase
   unsigned long long t_start, t_exhausted, t_end, dumped;  // globaltimer (stats variant), items dumped
   unsigned long long stats[8];
+  unsigned long long t_frac[8];  // stats variant: when the pose cursor passed k/8 of N
 };
 static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte workspace header");
 
@@ -640,6 +641,10 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
         unsigned base = 0;
         if (c.lane == 0) base = atomicAdd(&p.ctl->cursor[0], (unsigned)kGrab);
         base = __shfl_sync(FULL, base, 0);
+        if (STATS && c.lane == 0 && base < (unsigned)p.N) {
+          const unsigned long long f = (8ull * base) / (unsigned)p.N;
+          if (f != (8ull * (base + kGrab)) / (unsigned)p.N || base == 0) atomicMin(&p.ctl->t_frac[f], globaltimer_ns());
+        }
         if (base >= (unsigned)p.N) {
           poses_left = false;
           if (STATS && c.lane == 0) atomicMin(&p.ctl->t_exhausted, globaltimer_ns());
@@ -935,6 +940,7 @@ __global__ void init_kernel(Params p, int reset_stats) {
       p.ctl->t_exhausted = ~0ull;
       p.ctl->t_end = 0ull;
       p.ctl->dumped = 0ull;
+      for (int s = 0; s < 8; ++s) p.ctl->t_frac[s] = ~0ull;
     }
   }
 }
@@ -1219,6 +1225,8 @@ int cbvh_read_stats(const void* d_ws, cbvh_stats* out, void* stream) {
   out->kernel_ns = timed ? ctl.t_end - ctl.t_start : 0;
   out->tail_ns = (timed && ctl.t_exhausted != ~0ull && ctl.t_end >= ctl.t_exhausted) ? ctl.t_end - ctl.t_exhausted : 0;
   out->dumped = ctl.dumped;
+  for (int k = 0; k < 8; ++k)
+    out->timeline_ns[k] = (timed && ctl.t_frac[k] != ~0ull && ctl.t_frac[k] >= ctl.t_start) ? ctl.t_frac[k] - ctl.t_start : 0;
   return CBVH_OK;
 }
 
