@@ -85,7 +85,7 @@ constexpr int kFields = 16;         // words per stack entry
 constexpr int kLeafQ = 64;          // leaf-queue entries per warp
 constexpr int kSpillCap = 2048;     // global spill entries per warp
 constexpr int kContCap = 1 << 19;   // continuation-buffer items (per buffer, two buffers)
-constexpr int kGrabItems = 4;       // continuation items acquired per cursor atomic
+constexpr int kGrabItems = 1;       // continuation items acquired per cursor atomic
 constexpr int kGrab = 8;            // poses acquired per cursor atomic
 constexpr int kLowWater = 4;        // acquire poses when the stack is below this
 
@@ -104,6 +104,7 @@ struct Params {
   uint32_t* cont_in;     // continuation items of the previous phase [kContCap][kFields]
   uint32_t* cont_out;    // continuation items for the next phase
   int phase;             // 0: poses; >= 1: the previous phase's continuation items
+  int nwarps;            // warps in the grid
   int budget;            // iterations a warp may run after its input is exhausted (< 0: unbounded)
   int descent;           // CBVH_DESCENT_SIMULTANEOUS (Alg. 1 verbatim) or CBVH_DESCENT_LARGER
 };
@@ -638,18 +639,25 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
     // bounds the stack by the deepest single traversal, not the batch size)
     if (poses_left && top < kLowWater && spill_top == 0) {
       if (p.phase == 0) {
-        unsigned base = 0;
-        if (c.lane == 0) base = atomicAdd(&p.ctl->cursor[0], (unsigned)kGrab);
+        // chunks of kGrab poses while plenty remain, single poses near the end
+        // (a chunk of several heavy poses in one warp is the tail otherwise)
+        unsigned base = 0, g = 1;
+        if (c.lane == 0) {
+          const unsigned hint = __ldcg(&p.ctl->cursor[0]);
+          g = (hint + (unsigned)kGrab * (unsigned)p.nwarps * 8u < (unsigned)p.N) ? (unsigned)kGrab : 1u;
+          base = atomicAdd(&p.ctl->cursor[0], g);
+        }
         base = __shfl_sync(FULL, base, 0);
+        g = __shfl_sync(FULL, g, 0);
         if (STATS && c.lane == 0 && base < (unsigned)p.N) {
           const unsigned long long f = (8ull * base) / (unsigned)p.N;
-          if (f != (8ull * (base + kGrab)) / (unsigned)p.N || base == 0) atomicMin(&p.ctl->t_frac[f], globaltimer_ns());
+          if (f != (8ull * (base + g)) / (unsigned)p.N || base == 0) atomicMin(&p.ctl->t_frac[f], globaltimer_ns());
         }
         if (base >= (unsigned)p.N) {
           poses_left = false;
           if (STATS && c.lane == 0) atomicMin(&p.ctl->t_exhausted, globaltimer_ns());
         } else {
-          const int k = min(kGrab, p.N - (int)base);
+          const int k = min((int)g, p.N - (int)base);
           if (c.lane < k) {
             if (root_leafpair) {
               const int slot = nleaf + c.lane;
@@ -1081,6 +1089,7 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
   uint32_t* cont0 = p.spill + (size_t)s.warps * kSpillCap * kFields;
   uint32_t* cont1 = cont0 + (size_t)kContCap * kFields;
   p.descent = descent;
+  p.nwarps = s.warps;
   int ib = (int)((N + 255) / 256);
   ib = ib < 1 ? 1 : (ib > 4096 ? 4096 : ib);
   init_kernel<MODE><<<ib, 256, 0, st>>>(p, STATS ? 1 : 0);
