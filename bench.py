@@ -187,8 +187,13 @@ def run(args):
     w = G.make_config(args.config, num_poses=args.poses, pose_seed_offset=rank)
     N = len(w.poses)
     t0 = time.time()
+    if args.branching:
+        w.branching = args.branching
+    if args.bits:
+        w.bits = args.bits
     A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, w.leaf)
     B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, w.leaf)
+    distance = w.mode == "distance"
     build_s = time.time() - t0
     A.to_device(dev)
     B.to_device(dev)
@@ -196,13 +201,17 @@ def run(args):
     poses = poses_h.to(dev)
     hit = torch.empty(N, dtype=torch.uint8, device=dev)
     cnt = torch.empty(N, dtype=torch.int32, device=dev)
-    ws = M.Workspace(A, B, 0, dev)
+    dst = torch.empty(N, dtype=torch.float32, device=dev)
+    ws = M.Workspace(A, B, 1 if distance else 0, dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     lib = L.load()
 
-    def step():
-        M.collide_batch(A, B, poses, hit, cnt, ws)
+    def step(stats=False):
+        if distance:
+            M.distance_batch(A, B, poses, dst, ws, stats=stats, descent=args.descent)
+        else:
+            M.collide_batch(A, B, poses, hit, cnt, ws, stats=stats, descent=args.descent)
 
     # ---- warm-up (untimed)
     for _ in range(max(3, args.warmup)):
@@ -240,10 +249,10 @@ def run(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         T = float(t.item())
     value = N * args.steps * world / T
-    hits = int(hit.sum().item())
+    hits = 0 if distance else int(hit.sum().item())
 
     if args.quick:
-        M.collide_batch(A, B, poses, hit, cnt, ws, stats=True)
+        step(stats=True)
         st = M.read_stats(ws)
         if rank == 0:
             print(json.dumps({"quick": True, "value": value, "ms_per_step": 1e3 * T / args.steps,
@@ -255,7 +264,7 @@ def run(args):
         return
 
     # ---- stats run (untimed): BV-pair tests and algorithmic bytes per launch
-    M.collide_batch(A, B, poses, hit, cnt, ws, stats=True)
+    step(stats=True)
     st = M.read_stats(ws)
     kern_s = statistics.mean(kern_ms) / 1e3
     alg_bytes = st["record_bytes"] + st["tri_bytes"] + N * (48 + 5)
@@ -279,9 +288,12 @@ def run(args):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         poses.copy_(poses_h, non_blocking=True)
-        M.collide_batch(A, B, poses, hit, cnt, ws)
-        hit_h.copy_(hit, non_blocking=True)
-        cnt_h.copy_(cnt, non_blocking=True)
+        step()
+        if distance:
+            cnt_h.view(torch.float32).copy_(dst, non_blocking=True)
+        else:
+            hit_h.copy_(hit, non_blocking=True)
+            cnt_h.copy_(cnt, non_blocking=True)
         b.record(stream)
         b.synchronize()
         if k >= args.warmup:
@@ -298,7 +310,7 @@ def run(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": ("proximity queries (poses)/sec" if distance else METRIC), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": w.name, "poses_per_gpu": N, "A_tris": w.A.num_triangles,
@@ -312,13 +324,14 @@ def run(args):
             "bytes_per_node": {"A": A.info["bytes_per_node"], "B": B.info["bytes_per_node"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                         "kernel": "traverse_kernel<collide>", "kernel_ms": 1e3 * kern_s,
+                         "kernel": "traverse_kernel<%s> (all phases)" % ("distance" if distance else "collide"),
+                         "kernel_ms": 1e3 * kern_s,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "peak_source": peaks["_source"] + " hbm_gbs (copy bandwidth)"},
             "stats": st,
             "e2e": {"value": N * args.steps * world / E, "unit": UNIT,
                     "h2d_bytes_per_step": int(poses_h.numel() * 4),
-                    "d2h_bytes_per_step": int(N * (1 + 4))},
+                    "d2h_bytes_per_step": int(N * (4 if distance else 1 + 4))},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "build_s": build_s,
@@ -340,6 +353,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
     ap.add_argument("--quick", action="store_true", help="timed steps only (A/B comparisons)")
+    ap.add_argument("--branching", type=int, default=0, help="override B (config-3 sweep)")
+    ap.add_argument("--bits", type=int, default=0, help="override b (config-3 sweep)")
+    ap.add_argument("--descent", default="larger", choices=["larger", "simultaneous"])
     ap.add_argument("--cpu-poses", type=int, default=100000)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-poses", type=int, default=2048, help="poses per --impl reference step")
