@@ -395,6 +395,22 @@ __device__ __forceinline__ uint32_t pack_list(uint32_t m) {
   return list | (n << 8);
 }
 
+// Euclidean gap between the AABBs of two triangles (a lower bound on their
+// distance)
+__device__ __forceinline__ float tri_box_gap(const Tri& V, const Tri& U) {
+  float g2 = 0.f;
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float vlo = fminf(V.v[0][k], fminf(V.v[1][k], V.v[2][k]));
+    const float vhi = fmaxf(V.v[0][k], fmaxf(V.v[1][k], V.v[2][k]));
+    const float ulo = fminf(U.v[0][k], fminf(U.v[1][k], U.v[2][k]));
+    const float uhi = fmaxf(U.v[0][k], fmaxf(U.v[1][k], U.v[2][k]));
+    const float g = fmaxf(0.f, fmaxf(ulo - vhi, vlo - uhi));
+    g2 = fmaf(g, g, g2);
+  }
+  return sqrtf(g2);
+}
+
 // fp64 re-evaluation of a near-contact distance candidate,
 // in the world frame as the distance is defined: A's fp32
 // triangle mapped by the fp32 pose lifted exactly to fp64, B's fp32 triangle
@@ -421,7 +437,7 @@ __device__ __noinline__ float tri_dist_fp64(const PoseF& P, const float* trisA, 
 // the traversal kernel
 // ----------------------------------------------------------------------------
 
-constexpr int kWarpSmemWords = kFields * kStack + 4 * kLeafQ;
+constexpr int kWarpSmemWords = kFields * kStack + 5 * kLeafQ;
 
 // child pairs of an item: Alg. 1 enumerates children of every side it
 // descends (flags chosen at push time, see descent_flags)
@@ -450,7 +466,7 @@ __device__ __forceinline__ uint32_t full_mask(uint32_t t) { return (2u << ((t >>
 // per-warp constant context (registers); mutable counters live in the kernel
 struct WarpCtx {
   uint32_t* st;     // stack SoA [kFields][kStack]
-  uint32_t* lq;     // leaf queue SoA [4][kLeafQ]: pose, topoA, topoB, triangle masks (A bits 0-3, B bits 4-7)
+  uint32_t* lq;     // leaf queue SoA [5][kLeafQ]: pose, topoA, topoB, triangle lists, lower bound (distance)
   uint32_t* spill;  // this warp's global spill area [kSpillCap][kFields]
   int lane;
 };
@@ -472,6 +488,10 @@ __device__ __noinline__ unsigned drain_leaves(const Params& p, const WarpCtx c, 
       tb = c.lq[2 * kLeafQ + head + c.lane];
       mk = c.lq[3 * kLeafQ + head + c.lane];
       n = (int)((mk >> 8) & 7u) * (int)((mk >> 19) & 7u);  // only triangles the box filters kept
+      // distance: a leaf pair whose box bound no longer beats the pose's best
+      // distance (tightened since it was queued) is skipped
+      if (MODE == 1 && __uint_as_float(c.lq[4 * kLeafQ + head + c.lane]) >= __uint_as_float(__ldcg(&p.dist_bits[pose])))
+        n = 0;
     }
     int incl = n;
     #pragma unroll
@@ -507,12 +527,19 @@ __device__ __noinline__ unsigned drain_leaves(const Params& p, const WarpCtx c, 
         // triangles whose AABBs are disjoint cannot intersect
         hit = tri_boxes_overlap(TA, TB) && tri_tri_overlap(TA, TB);
       } else {
+        // triangle AABB gap: a lower bound; skip pairs that cannot beat the best
+        const float tmax0 = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
+        const float best = __uint_as_float(__ldcg(&p.dist_bits[my_pose]));
+        if (tri_box_gap(TA, TB) - 2e-6f * (tmax0 + p.A.maxabs + p.B.maxabs) >= best) {
+          d = FLT_MAX;
+        } else {
         d = tri_tri_dist(TA, TB);
         // fp32 error here is ~1e-7 x (|t| + model extents); candidates whose
         // distance is too small for a 1e-5 relative bound are re-evaluated in
         // fp64
         const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
         if (d < 0.05f * (tmax + p.A.maxabs + p.B.maxabs)) d = tri_dist_fp64(P, p.A.tris, ia, p.B.tris, ib);
+        }
       }
     }
     tests += (unsigned)total;
@@ -665,6 +692,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
               c.lq[1 * kLeafQ + slot] = p.A.root_topo;
               c.lq[2 * kLeafQ + slot] = p.B.root_topo;
               c.lq[3 * kLeafQ + slot] = pack_list(full_mask(p.A.root_topo)) | (pack_list(full_mask(p.B.root_topo)) << 11);
+              c.lq[4 * kLeafQ + slot] = 0u;
             } else {
               const int slot = top + c.lane;
               c.st[F_POSE * kStack + slot] =
@@ -884,6 +912,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
           c.lq[1 * kLeafQ + s2] = cta;
           c.lq[2 * kLeafQ + s2] = ctb;
           c.lq[3 * kLeafQ + s2] = pack_list(mskA & full_mask(cta)) | (pack_list(mskB & full_mask(ctb)) << 11);
+          if (MODE == 1) c.lq[4 * kLeafQ + s2] = __float_as_uint(lb);
         }
         nleaf += __popc(lm);
         if (STATS) {
