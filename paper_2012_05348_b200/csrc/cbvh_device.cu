@@ -502,8 +502,12 @@ __device__ __noinline__ unsigned drain_leaves(const Params& p, const WarpCtx c, 
     const unsigned fit = __ballot_sync(FULL, c.lane < avail && incl <= 32);
     const int m = __popc(fit);  // >= 2: an entry has at most 16 triangle pairs
     const int total = __shfl_sync(FULL, incl, m - 1);
-    const unsigned starts = __reduce_or_sync(FULL, (c.lane < m) ? (1u << (incl - n)) : 0u);
-    int e = __popc(starts & ((2u << c.lane) - 1u)) - 1;
+    // lane -> entry: rank among the non-empty entries (empty ones — distance
+    // pairs pruned above — share a start position with their successor)
+    const unsigned nz = __ballot_sync(FULL, c.lane < m && n > 0);
+    const unsigned starts = __reduce_or_sync(FULL, (c.lane < m && n > 0) ? (1u << (incl - n)) : 0u);
+    const int r = __popc(starts & ((2u << c.lane) - 1u)) - 1;
+    const int e = (nz != 0u && r >= 0) ? (int)__fns(nz, 0, r + 1) : 0;
     const int start_e = __shfl_sync(FULL, incl - n, e);
     const uint32_t my_pose = __shfl_sync(FULL, pose, e);
     const uint32_t my_ta = __shfl_sync(FULL, ta, e);
