@@ -108,6 +108,27 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def rank_workload(config: int, rank: int, num_poses=None):
+    """Weak-scaling shard: every rank gets the same meshes and its own
+    independent, equally sized pose batch (pose seed offset = rank)."""
+    return G.make_config(config, num_poses=num_poses, pose_seed_offset=rank)
+
+
+def max_over_ranks(seconds: float, dist=None, device=None) -> float:
+    """The job's time is the slowest rank's (max all-reduce); no-op at N=1."""
+    if dist is None:
+        return seconds
+    import torch
+    t = torch.tensor([seconds], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_rate(units_per_rank: int, steps: int, world: int, seconds: float) -> float:
+    """Whole-job throughput: units all ranks processed / max-over-ranks time."""
+    return units_per_rank * steps * world / seconds
+
+
 def cpu_oracle_rate(w, n_sample: int, nthreads: int = 0, budget_s: float = 25.0):
     """The fp64 oracle (as it stands) on a bounded prefix of the workload's poses."""
     import oracle as O
@@ -184,7 +205,7 @@ def run(args):
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
 
-    w = G.make_config(args.config, num_poses=args.poses, pose_seed_offset=rank)
+    w = rank_workload(args.config, rank, args.poses)
     N = len(w.poses)
     t0 = time.time()
     if args.branching:
@@ -243,12 +264,8 @@ def run(args):
     M.check(ws)
     step_ms = [a.elapsed_time(b) for a, b in ev]
     kern_ms = [a.elapsed_time(b) for a, b in kev]
-    T = sum(step_ms) / 1e3
-    if dist:
-        t = torch.tensor([T], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        T = float(t.item())
-    value = N * args.steps * world / T
+    T = max_over_ranks(sum(step_ms) / 1e3, dist, dev)
+    value = aggregate_rate(N, args.steps, world, T)
     hits = 0 if distance else int(hit.sum().item())
 
     if args.quick:
@@ -298,11 +315,7 @@ def run(args):
         b.synchronize()
         if k >= args.warmup:
             e2e_ms.append(a.elapsed_time(b))
-    E = sum(e2e_ms) / 1e3
-    if dist:
-        t = torch.tensor([E], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        E = float(t.item())
+    E = max_over_ranks(sum(e2e_ms) / 1e3, dist, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -329,7 +342,7 @@ def run(args):
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "peak_source": peaks["_source"] + " hbm_gbs (copy bandwidth)"},
             "stats": st,
-            "e2e": {"value": N * args.steps * world / E, "unit": UNIT,
+            "e2e": {"value": aggregate_rate(N, args.steps, world, E), "unit": UNIT,
                     "h2d_bytes_per_step": int(poses_h.numel() * 4),
                     "d2h_bytes_per_step": int(N * (4 if distance else 1 + 4))},
             "gpu_launches": launches,
