@@ -76,6 +76,12 @@ struct Control {
 };
 static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte workspace header");
 
+#ifndef CBVH_DESCENT_BOTH
+#define CBVH_DESCENT_BOTH 1.0f
+#endif
+#ifndef CBVH_DESCENT_METRIC
+#define CBVH_DESCENT_METRIC 0
+#endif
 #ifndef CBVH_MIN_BLOCKS
 #define CBVH_MIN_BLOCKS 4
 #endif
@@ -455,8 +461,16 @@ __device__ __forceinline__ uint32_t descent_flags(int rule, uint32_t ta, uint32_
                                                   const int32_t CB[6], float cellA, float cellB) {
   const bool ai = !(ta & kLeafBit), bi = !(tb & kLeafBit);
   if (!(ai && bi) || rule == 0) return (ai ? kDescA : 0u) | (bi ? kDescB : 0u);
+#if CBVH_DESCENT_METRIC == 1
+  // max extent
+  const float ea = (float)max(CA[3] - CA[0], max(CA[4] - CA[1], CA[5] - CA[2])) * cellA;
+  const float eb = (float)max(CB[3] - CB[0], max(CB[4] - CB[1], CB[5] - CB[2])) * cellB;
+#else
   const float ea = (float)((CA[3] - CA[0]) + (CA[4] - CA[1]) + (CA[5] - CA[2])) * cellA;
   const float eb = (float)((CB[3] - CB[0]) + (CB[4] - CB[1]) + (CB[5] - CB[2])) * cellB;
+#endif
+  // similar sizes (within CBVH_DESCENT_BOTH): descend both, as Alg. 1 does
+  if (ea < CBVH_DESCENT_BOTH * eb && eb < CBVH_DESCENT_BOTH * ea) return kDescA | kDescB;
   return ea >= eb ? kDescA : kDescB;
 }
 

@@ -1,7 +1,15 @@
 #!/bin/bash
-# A/B timing of library variants on the same box: tools/ab.sh lib1.so lib2.so ...
-for v in "$@"; do
-  for rep in 1 2; do
-    CBVH_LIB=$PWD/paper_2012_05348_b200/$v timeout 600 python bench.py --steps 10 --warmup 3 --quick "${AB_ARGS[@]}" 2>&1 | tail -1
+# A/B timing of library variants on the same box: CONFIGS="5 3" tools/ab.sh lib1.so lib2.so ...
+CONFIGS=${CONFIGS:-5}
+for cfg in $CONFIGS; do
+  for v in "$@"; do
+    CBVH_LIB=$PWD/paper_2012_05348_b200/$v timeout 600 python bench.py --config $cfg --steps 5 --warmup 3 --quick 2>&1 | tail -1 | python -c "
+import sys, json
+l = sys.stdin.read().strip()
+try:
+    d = json.loads(l); print('cfg$cfg', '$v', round(d['ms_per_step'], 3), 'ms', round(d['value'] / 1e6, 3), 'M/s')
+except Exception:
+    print('cfg$cfg', '$v', 'FAILED', l[-300:])
+"
   done
 done
