@@ -277,7 +277,9 @@ def run(args):
                               "lib": os.environ.get("CBVH_LIB", "default"),
                               "stats_kernel_ms": st["kernel_ns"] / 1e6, "stats_tail_ms": st["tail_ns"] / 1e6,
                               "dumped": st["dumped"], "launches": M.last_launch_count(),
-                              "timeline_ms": [t / 1e6 for t in st["timeline_ns"]]}), flush=True)
+                              "timeline_ms": [t / 1e6 for t in st["timeline_ns"]],
+                              "lane_util": st["bv_tests"] / max(1, 32 * st["iterations"]),
+                              "iterations": st["iterations"], "bv_tests": st["bv_tests"]}), flush=True)
         return
 
     # ---- stats run (untimed): BV-pair tests and algorithmic bytes per launch

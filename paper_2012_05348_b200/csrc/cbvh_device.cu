@@ -73,6 +73,7 @@ struct Control {
   unsigned long long t_start, t_exhausted, t_end, dumped;  // globaltimer (stats variant), items dumped
   unsigned long long stats[8];
   unsigned long long t_frac[8];  // stats variant: when the pose cursor passed k/8 of N
+  unsigned long long iterations; // stats variant: expansion passes (warp iterations)
 };
 static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte workspace header");
 
@@ -92,8 +93,14 @@ constexpr int kLeafQ = 64;          // leaf-queue entries per warp
 constexpr int kSpillCap = 2048;     // global spill entries per warp
 constexpr int kContCap = 1 << 19;   // continuation-buffer items (per buffer, two buffers)
 constexpr int kGrabItems = 1;       // continuation items acquired per cursor atomic
-constexpr int kGrab = 8;            // poses acquired per cursor atomic
-constexpr int kLowWater = 4;        // acquire poses when the stack is below this
+#ifndef CBVH_GRAB
+#define CBVH_GRAB 8
+#endif
+#ifndef CBVH_LOW_WATER
+#define CBVH_LOW_WATER 4
+#endif
+constexpr int kGrab = CBVH_GRAB;          // poses acquired per cursor atomic
+constexpr int kLowWater = CBVH_LOW_WATER; // acquire poses when the stack is below this
 
 // stack fields
 enum { F_POSE = 0, F_TA = 1, F_TB = 2, F_BA = 3, F_BB = 9, F_LB = 15 };
@@ -392,6 +399,94 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
   return m;
 }
 
+#ifndef CBVH_FILTER_TASKS
+#define CBVH_FILTER_TASKS 0
+#endif
+#ifndef CBVH_TASKS_INLINE
+#define CBVH_TASKS_INLINE 1
+#endif
+#if CBVH_TASKS_INLINE
+#define CBVH_TASKS_ATTR __forceinline__
+#else
+#define CBVH_TASKS_ATTR __noinline__
+#endif
+
+// Warp-dense leaf refinement: every (surviving child pair, triangle of a leaf
+// side) test of the warp becomes one task; tasks are spread over the 32 lanes
+// in rounds (the per-lane loop left ~60 % of the lanes idle).  A lane needing
+// the B-side test (its A box vs B leaf ctb's triangles, in A's frame) owns
+// ntri(ctb) tasks, then ntri(cta) tasks for the A side (B box vs A leaf cta's
+// triangles, in the world).  Returns the refined survival; masks per side.
+__device__ CBVH_TASKS_ATTR bool leaf_filter_tasks(const Params& p, int lane, bool surv, uint32_t pose, uint32_t cta,
+                                               uint32_t ctb, const float alo[3], const float ahi[3],
+                                               const float blo[3], const float bhi[3], float eps,
+                                               uint32_t* mskA, uint32_t* mskB) {
+  const bool needB = surv && (ctb & kLeafBit), needA = surv && (cta & kLeafBit);
+  const int tB = needB ? (int)((ctb >> 29) & 3u) + 1 : 0;
+  const int tA = needA ? (int)((cta >> 29) & 3u) + 1 : 0;
+  const int t = tB + tA;
+  int incl = t;
+  #pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int off = incl - t;
+  const int total = __shfl_sync(FULL, incl, 31);
+  uint32_t bits = 0;
+  for (int r0 = 0; r0 < total; r0 += 32) {
+    // owner of task r0 + lane: lanes whose range starts in this round, or the
+    // one whose range runs into it from the previous round
+    const bool begins = t > 0 && off >= r0 && off < r0 + 32;
+    const unsigned bm = __ballot_sync(FULL, begins);
+    const unsigned starts = __reduce_or_sync(FULL, begins ? (1u << (off - r0)) : 0u);
+    const unsigned carry = __ballot_sync(FULL, t > 0 && off < r0 && off + t > r0);
+    const int nst = __popc(starts & ((2u << lane) - 1u));
+    const int owner = nst == 0 ? (carry ? __ffs(carry) - 1 : 0) : (int)__fns(bm, 0, nst);
+    const int o_off = __shfl_sync(FULL, off, owner);
+    const int o_tB = __shfl_sync(FULL, tB, owner);
+    const uint32_t o_pose = __shfl_sync(FULL, pose, owner);
+    const uint32_t o_leafB = __shfl_sync(FULL, ctb, owner), o_leafA = __shfl_sync(FULL, cta, owner);
+    const float o_eps = __shfl_sync(FULL, eps, owner);
+    const int j = r0 + lane - o_off;
+    const bool dir0 = j < o_tB;
+    float lo[3], hi[3];
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float a0 = __shfl_sync(FULL, alo[k], owner), a1 = __shfl_sync(FULL, ahi[k], owner);
+      const float b0 = __shfl_sync(FULL, blo[k], owner), b1 = __shfl_sync(FULL, bhi[k], owner);
+      lo[k] = dir0 ? a0 : b0;
+      hi[k] = dir0 ? a1 : b1;
+    }
+    bool ok = false;
+    if (r0 + lane < total) {
+      const PoseF P = load_pose(p.poses, (int)o_pose);
+      float cc[3], hh[3];
+      #pragma unroll
+      for (int k = 0; k < 3; ++k) { cc[k] = 0.5f * (lo[k] + hi[k]); hh[k] = 0.5f * (hi[k] - lo[k]); }
+      Tri W;
+      if (dir0) {
+        W = to_local(P, load_tri(p.B.tris, (o_leafB & 0x1FFFFFFFu) + (uint32_t)j));
+      } else {
+        const Tri L = load_tri(p.A.tris, (o_leafA & 0x1FFFFFFFu) + (uint32_t)(j - o_tB));
+        #pragma unroll
+        for (int v = 0; v < 3; ++v)
+          #pragma unroll
+          for (int k = 0; k < 3; ++k)
+            W.v[v][k] = fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], P.t[k])));
+      }
+      ok = box_tri_overlap(cc, hh, W, o_eps);
+    }
+    const unsigned rb = __ballot_sync(FULL, ok);
+    const int lo_i = max(off, r0), hi_i = min(off + t, r0 + 32);
+    if (t > 0 && lo_i < hi_i) bits |= ((rb >> (lo_i - r0)) & ((2u << (hi_i - lo_i - 1)) - 1u)) << (lo_i - off);
+  }
+  const uint32_t mb = bits & ((1u << tB) - 1u), ma = (bits >> tB) & ((1u << tA) - 1u);
+  *mskB = needB ? mb : 15u;
+  *mskA = needA ? ma : 15u;
+  return surv && (!needB || mb != 0u) && (!needA || ma != 0u);
+}
+
 // packed list of the set bits of a <= 4-bit mask: 2-bit indices, count
 __device__ __forceinline__ uint32_t pack_list(uint32_t m) {
   uint32_t list = 0, n = 0;
@@ -670,7 +765,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * kFields;
   int top = 0, nleaf = 0, spill_top = 0;
   int after = 0;  // iterations since the input ran out
-  unsigned long long s_dump = 0;
+  unsigned long long s_dump = 0, s_iter = 0;
   unsigned long long s_bv = 0, s_exp = 0, s_leaf = 0, s_tri = 0, s_dec = 0, s_rec = 0, s_lbytes = 0, s_spill = 0;
   bool poses_left = true;
   const unsigned lt = lanemask_lt();
@@ -817,7 +912,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
     const float item_lb = __uint_as_float(c.st[F_LB * kStack + slot]);
     __syncwarp();
     top -= m;
-    if (STATS) s_exp += m;
+    if (STATS) { s_exp += m; s_iter += passes; }
 
     const PoseF P = load_pose(p.poses, (int)pose);
     const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
@@ -837,6 +932,9 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
       bool surv = false;
       float lb = 0.f;
       uint32_t mskA = 15u, mskB = 15u;
+#if CBVH_FILTER_TASKS
+      float alo_s[3] = {0.f, 0.f, 0.f}, ahi_s[3] = {0.f, 0.f, 0.f}, blo_s[3] = {0.f, 0.f, 0.f}, bhi_s[3] = {0.f, 0.f, 0.f};
+#endif
       if (valid) {
         if (a_int) {
           const uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
@@ -861,6 +959,10 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
         float alo[3], ahi[3], blo[3], bhi[3];
         to_float_box(p.A, CA, alo, ahi);
         to_float_box(p.B, CB, blo, bhi);
+#if CBVH_FILTER_TASKS
+        #pragma unroll
+        for (int k = 0; k < 3; ++k) { alo_s[k] = alo[k]; ahi_s[k] = ahi[k]; blo_s[k] = blo[k]; bhi_s[k] = bhi[k]; }
+#endif
         if (MODE == 0) {
           surv = sat_gap<false>(P, alo, ahi, blo, bhi, eps, nullptr) <= 0.f;
           // Against a leaf, "intersect" is refined to the leaf's triangles
@@ -869,6 +971,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
           // box alone lets every A leaf crossing a B leaf box through.  For a
           // leaf pair both sides are filtered and the surviving triangles are
           // recorded as masks for the leaf phase.
+#if !CBVH_FILTER_TASKS
           if (surv && (ctb & kLeafBit)) {
             mskB = box_hits_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps);
             surv = mskB != 0u;
@@ -877,6 +980,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
             mskA = box_hits_leaf<1>(P, blo, bhi, p.A.tris, cta, eps);
             surv = mskA != 0u;
           }
+#endif
         } else {
           sat_gap<true>(P, alo, ahi, blo, bhi, eps, &lb);
           surv = lb < best;
@@ -887,6 +991,14 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
         }
       }
       if (STATS) s_bv += __popc(__ballot_sync(FULL, valid)) * (c.lane == 0 ? 1 : 0);
+#if CBVH_FILTER_TASKS
+      if (MODE == 0) {
+        uint32_t ma, mb;
+        surv = leaf_filter_tasks(p, c.lane, surv, pose, cta, ctb, alo_s, ahi_s, blo_s, bhi_s, eps, &ma, &mb);
+        mskA = ma;
+        mskB = mb;
+      }
+#endif
       const bool leafpair = surv && (cta & kLeafBit) && (ctb & kLeafBit);
       const bool push = surv && !leafpair;
       // ---- ballot/popc compaction: internal pairs back onto the stack
@@ -971,6 +1083,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
       atomicAdd(&p.ctl->stats[6], lb);
       atomicAdd(&p.ctl->stats[7], s_spill);
       atomicAdd(&p.ctl->dumped, s_dump);
+      atomicAdd(&p.ctl->iterations, s_iter);
     }
   }
 }
@@ -995,6 +1108,7 @@ __global__ void init_kernel(Params p, int reset_stats) {
       p.ctl->t_exhausted = ~0ull;
       p.ctl->t_end = 0ull;
       p.ctl->dumped = 0ull;
+      p.ctl->iterations = 0ull;
       for (int s = 0; s < 8; ++s) p.ctl->t_frac[s] = ~0ull;
     }
   }
@@ -1281,6 +1395,7 @@ int cbvh_read_stats(const void* d_ws, cbvh_stats* out, void* stream) {
   out->kernel_ns = timed ? ctl.t_end - ctl.t_start : 0;
   out->tail_ns = (timed && ctl.t_exhausted != ~0ull && ctl.t_end >= ctl.t_exhausted) ? ctl.t_end - ctl.t_exhausted : 0;
   out->dumped = ctl.dumped;
+  out->iterations = ctl.iterations;
   for (int k = 0; k < 8; ++k)
     out->timeline_ns[k] = (timed && ctl.t_frac[k] != ~0ull && ctl.t_frac[k] >= ctl.t_start) ? ctl.t_frac[k] - ctl.t_start : 0;
   return CBVH_OK;
