@@ -87,7 +87,10 @@ static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte works
 #define CBVH_MIN_BLOCKS 4
 #endif
 constexpr int kWarps = 4;           // warps per CTA
-constexpr int kStack = 64;          // smem stack entries per warp
+#ifndef CBVH_STACK
+#define CBVH_STACK 64
+#endif
+constexpr int kStack = CBVH_STACK;  // smem stack entries per warp
 constexpr int kFields = 16;         // words per stack entry
 constexpr int kLeafQ = 64;          // leaf-queue entries per warp
 constexpr int kSpillCap = 2048;     // global spill entries per warp
@@ -399,6 +402,9 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
   return m;
 }
 
+#ifndef CBVH_LEAFPAIR_ONE_SIDE
+#define CBVH_LEAFPAIR_ONE_SIDE 0
+#endif
 #ifndef CBVH_FILTER_TASKS
 #define CBVH_FILTER_TASKS 0
 #endif
@@ -972,11 +978,22 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
           // leaf pair both sides are filtered and the surviving triangles are
           // recorded as masks for the leaf phase.
 #if !CBVH_FILTER_TASKS
-          if (surv && (ctb & kLeafBit)) {
+#if CBVH_LEAFPAIR_ONE_SIDE
+          // a leaf pair refines only the larger leaf's side (the smaller
+          // leaf's few triangles rarely reject the larger box)
+          const bool lpair = (cta & kLeafBit) && (ctb & kLeafBit);
+          const float exa = (ahi[0] - alo[0]) + (ahi[1] - alo[1]) + (ahi[2] - alo[2]);
+          const float exb = (bhi[0] - blo[0]) + (bhi[1] - blo[1]) + (bhi[2] - blo[2]);
+          const bool doB = (ctb & kLeafBit) && (!lpair || exb >= exa);
+          const bool doA = (cta & kLeafBit) && (!lpair || exa > exb);
+#else
+          const bool doB = (ctb & kLeafBit) != 0, doA = (cta & kLeafBit) != 0;
+#endif
+          if (surv && doB) {
             mskB = box_hits_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps);
             surv = mskB != 0u;
           }
-          if (surv && (cta & kLeafBit)) {
+          if (surv && doA) {
             mskA = box_hits_leaf<1>(P, blo, bhi, p.A.tris, cta, eps);
             surv = mskA != 0u;
           }
