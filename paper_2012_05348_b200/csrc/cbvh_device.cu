@@ -88,7 +88,7 @@ static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte works
 #endif
 constexpr int kWarps = 4;           // warps per CTA
 #ifndef CBVH_STACK
-#define CBVH_STACK 64
+#define CBVH_STACK 96
 #endif
 constexpr int kStack = CBVH_STACK;  // smem stack entries per warp
 constexpr int kFields = 16;         // words per stack entry
