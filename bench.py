@@ -212,8 +212,8 @@ def run(args):
         w.branching = args.branching
     if args.bits:
         w.bits = args.bits
-    A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, w.leaf)
-    B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, w.leaf)
+    A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout)
+    B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout)
     distance = w.mode == "distance"
     build_s = time.time() - t0
     A.to_device(dev)
@@ -279,7 +279,8 @@ def run(args):
                               "dumped": st["dumped"], "launches": M.last_launch_count(),
                               "timeline_ms": [t / 1e6 for t in st["timeline_ns"]],
                               "lane_util": st["bv_tests"] / max(1, 32 * st["iterations"]),
-                              "iterations": st["iterations"], "bv_tests": st["bv_tests"]}), flush=True)
+                              "iterations": st["iterations"], "bv_tests": st["bv_tests"], "layout": args.layout,
+                              "bytes_per_node": {"A": A.info["bytes_per_node"], "B": B.info["bytes_per_node"]}}), flush=True)
         return
 
     # ---- stats run (untimed): BV-pair tests and algorithmic bytes per launch
@@ -330,7 +331,7 @@ def run(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": w.name, "poses_per_gpu": N, "A_tris": w.A.num_triangles,
                        "B_tris": w.B.num_triangles, "branching": w.branching, "bits": w.bits,
-                       "treelet_nodes": w.treelet, "leaf_size": w.leaf,
+                       "treelet_nodes": w.treelet, "leaf_size": w.leaf, "layout": args.layout,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"pose-sharded x{world} (independent batches)"},
             "bv_pair_tests_per_s": st["bv_tests"] / (statistics.median(step_ms) / 1e3),
@@ -371,6 +372,8 @@ def main():
     ap.add_argument("--branching", type=int, default=0, help="override B (config-3 sweep)")
     ap.add_argument("--bits", type=int, default=0, help="override b (config-3 sweep)")
     ap.add_argument("--descent", default="larger", choices=["larger", "simultaneous"])
+    ap.add_argument("--layout", default="delta", choices=["delta", "fp16", "fp32"],
+                    help="node box layout (fp16/fp32: the paper's half-vs-float ablation)")
     ap.add_argument("--cpu-poses", type=int, default=100000)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-poses", type=int, default=2048, help="poses per --impl reference step")

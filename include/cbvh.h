@@ -56,9 +56,16 @@ typedef struct {
   int64_t num_triangles;
 } cbvh_mesh;
 
+/* Node box layouts.  DELTA is the paper's compressed layout
+ * (b-bit corrections vs the decoded parent, §III.B / P:105); FP16 and
+ * FP32 store absolute boxes — binary16 rounded outward (§III.A) and
+ * exact single precision — for the paper's half-vs-float comparison. */
+enum { CBVH_LAYOUT_DELTA = 0, CBVH_LAYOUT_FP16 = 1, CBVH_LAYOUT_FP32 = 2 };
+
 typedef struct {
   int treelet_nodes; /* T: nodes per treelet ("clustering BVHs into smaller parts"); default 32; must be >= branching */
   int leaf_size;     /* c: max triangles per leaf, 1..4; default 4 */
+  int layout;        /* CBVH_LAYOUT_*; default CBVH_LAYOUT_DELTA (bits is ignored for FP16 / FP32) */
 } cbvh_build_opts;
 
 /* Build the compressed BVH of one mesh ("splitting the models and wrap it
@@ -87,6 +94,7 @@ typedef struct {
   float origin[3];
   int32_t root_box[6]; /* lattice lo xyz, hi xyz of the root */
   uint64_t off_topo, off_codes, off_treelets, off_tris, off_tri_index, total_bytes;
+  uint32_t layout;     /* CBVH_LAYOUT_* */
 } cbvh_header;
 
 typedef struct {
@@ -94,7 +102,7 @@ typedef struct {
   uint64_t bvh_bytes;      /* topo + codes + treelet table: the compressed hierarchy */
   uint64_t tri_bytes;      /* leaf-ordered fp32 triangle soup (48 B / triangle: 9 floats + 3 pads) */
   double bytes_per_node;   /* bvh_bytes / num_nodes */
-  double code_bytes_per_node; /* the BV descriptor alone: 6 * code_width / 8 */
+  double code_bytes_per_node; /* the BV descriptor alone: 6 * code_width / 8 (3 / 6 / 12 delta, 12 fp16, 24 fp32) */
 } cbvh_info;
 
 /* Validate and describe a host blob.  Errors: CBVH_EINVAL (null), CBVH_EBLOB. */

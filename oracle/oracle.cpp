@@ -325,12 +325,13 @@ struct BlobView {
   float origin[3];
   int32_t root[6];
   uint64_t off_topo, off_codes, off_treelets, off_tris, off_tri_index, total;
+  uint32_t layout;  // 0 delta (lattice corrections), 1 absolute binary16, 2 absolute fp32
 };
 
 template <class X> X rd(const uint8_t* p, size_t off) { X x; std::memcpy(&x, p + off, sizeof(X)); return x; }
 
 bool parse_blob(const uint8_t* p, size_t bytes, BlobView* b) {
-  if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0 || rd<uint32_t>(p, 4) != 2) return false;
+  if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0 || rd<uint32_t>(p, 4) != 3) return false;
   b->p = p; b->bytes = bytes;
   b->B = rd<uint32_t>(p, 8); b->bits = rd<uint32_t>(p, 12); b->T = rd<uint32_t>(p, 16);
   b->c = rd<uint32_t>(p, 20); b->w = rd<uint32_t>(p, 24); b->n_nodes = rd<uint32_t>(p, 28);
@@ -340,9 +341,36 @@ bool parse_blob(const uint8_t* p, size_t bytes, BlobView* b) {
   for (int a = 0; a < 6; ++a) b->root[a] = rd<int32_t>(p, 64 + 4 * a);
   b->off_topo = rd<uint64_t>(p, 88); b->off_codes = rd<uint64_t>(p, 96); b->off_treelets = rd<uint64_t>(p, 104);
   b->off_tris = rd<uint64_t>(p, 112); b->off_tri_index = rd<uint64_t>(p, 120); b->total = rd<uint64_t>(p, 128);
+  b->layout = rd<uint32_t>(p, 136);
   if (b->total != bytes) return false;
-  if (b->w != 4 && b->w != 8 && b->w != 16) return false;
+  if (b->layout == 0 && b->w != 4 && b->w != 8 && b->w != 16) return false;
+  if (b->layout == 1 && b->w != 16) return false;
+  if (b->layout == 2 && b->w != 32) return false;
+  if (b->layout > 2) return false;
   return true;
+}
+
+// IEEE binary16 -> double, from the bit layout (1 sign, 5 exponent, 10 mantissa).
+double half_to_double(uint16_t h) {
+  const int e = (h >> 10) & 31, m = h & 1023;
+  double v;
+  if (e == 0) v = std::ldexp((double)m, -24);
+  else if (e == 31) v = m ? std::numeric_limits<double>::quiet_NaN() : std::numeric_limits<double>::infinity();
+  else v = std::ldexp((double)(m + 1024), e - 25);
+  return (h & 0x8000) ? -v : v;
+}
+
+// Absolute box of node n in the FP16 / FP32 layouts (lo xyz, hi xyz).
+void abs_box(const BlobView& b, uint32_t n, double* lo, double* hi) {
+  for (int a = 0; a < 3; ++a) {
+    if (b.layout == 2) {
+      lo[a] = (double)rd<float>(b.p, b.off_codes + 24ull * n + 4 * a);
+      hi[a] = (double)rd<float>(b.p, b.off_codes + 24ull * n + 12 + 4 * a);
+    } else {
+      lo[a] = half_to_double(rd<uint16_t>(b.p, b.off_codes + 12ull * n + 2 * a));
+      hi[a] = half_to_double(rd<uint16_t>(b.p, b.off_codes + 12ull * n + 6 + 2 * a));
+    }
+  }
 }
 
 uint32_t blob_topo(const BlobView& b, uint32_t n) { return rd<uint32_t>(b.p, b.off_topo + 4ull * n); }
@@ -395,7 +423,11 @@ bool tree_from_blob(const BlobView& b, Tree& t, bool exact_boxes) {
     seen[n] = 1;
     order.push_back(n);
     Node& nd = t.nodes[n];
-    for (int a = 0; a < 3; ++a) { nd.lo[a] = lat(b, a, box[6ull * n + a]); nd.hi[a] = lat(b, a, box[6ull * n + 3 + a]); }
+    if (b.layout == 0) {
+      for (int a = 0; a < 3; ++a) { nd.lo[a] = lat(b, a, box[6ull * n + a]); nd.hi[a] = lat(b, a, box[6ull * n + 3 + a]); }
+    } else {
+      abs_box(b, n, nd.lo, nd.hi);
+    }
     uint32_t tp = blob_topo(b, n);
     if (tp >> 31) {
       uint32_t first = tp & 0x1FFFFFFFu, cnt = ((tp >> 29) & 3u) + 1;
@@ -857,12 +889,20 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
         if (ch >= b.n_nodes) { report[0]++; continue; }
         if (parent[ch] != -1) { report[0]++; continue; }
         parent[ch] = (int)n;
-        blob_codes(b, ch, q);
-        for (int f = 0; f < 6; ++f) if (q[f] >> b.bits) report[0]++;
-        decode_child(Pn, q, b.bits, &box[6ull * ch]);
-        const int64_t* C = &box[6ull * ch];
-        for (int a = 0; a < 3; ++a)
-          if (C[a] < Pn[a] || C[3 + a] > Pn[3 + a] || C[a] > C[3 + a]) report[2]++;
+        if (b.layout == 0) {
+          blob_codes(b, ch, q);
+          for (int f = 0; f < 6; ++f) if (q[f] >> b.bits) report[0]++;
+          decode_child(Pn, q, b.bits, &box[6ull * ch]);
+          const int64_t* C = &box[6ull * ch];
+          for (int a = 0; a < 3; ++a)
+            if (C[a] < Pn[a] || C[3 + a] > Pn[3 + a] || C[a] > C[3 + a]) report[2]++;
+        } else {
+          double plo[3], phi[3], clo[3], chi[3];
+          abs_box(b, n, plo, phi);
+          abs_box(b, ch, clo, chi);
+          for (int a = 0; a < 3; ++a)
+            if (clo[a] < plo[a] || chi[a] > phi[a] || clo[a] > chi[a]) report[2]++;
+        }
         stack.push_back(ch);
       }
     }
@@ -875,11 +915,17 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
       auto& dst = subtree_tris[parent[n]];
       dst.insert(dst.end(), subtree_tris[n].begin(), subtree_tris[n].end());
     }
+    double nlo[3], nhi[3];
+    if (b.layout == 0) {
+      for (int a = 0; a < 3; ++a) { nlo[a] = lat(b, a, box[6ull * n + a]); nhi[a] = lat(b, a, box[6ull * n + 3 + a]); }
+    } else {
+      abs_box(b, n, nlo, nhi);
+    }
     for (uint32_t ti : subtree_tris[n])
       for (int v = 0; v < 3; ++v)
         for (int a = 0; a < 3; ++a) {
           double x = (double)verts[3 * tris[3 * ti + v] + a];
-          if (x < lat(b, a, box[6ull * n + a]) || x > lat(b, a, box[6ull * n + 3 + a])) report[1]++;
+          if (x < nlo[a] || x > nhi[a]) report[1]++;
         }
     if (parent[n] >= 0) subtree_tris[n].clear(), subtree_tris[n].shrink_to_fit();
   }
@@ -906,8 +952,9 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
       bool in_root_group = (p == pf);
       if (!in_root_group && (p < 0 || treelet_of[p] != (int)k)) report[7]++;
     }
+    // anchors re-anchor the delta layout; absolute layouts need none
     const int64_t* ab = (pf < 0) ? nullptr : &box[6ull * pf];
-    for (int a = 0; a < 6; ++a) {
+    for (int a = 0; a < 6 && b.layout == 0; ++a) {
       int64_t want = ab ? ab[a] : (int64_t)b.root[a];
       if (anchor[a] != want) report[7]++;
     }

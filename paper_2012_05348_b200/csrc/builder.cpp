@@ -115,6 +115,39 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
+// Directed rounding to IEEE binary16 by search over the sorted table of all
+// finite half values (obviously correct; used once per node at build time).
+static const std::vector<std::pair<double, uint16_t>>& half_table() {
+  static std::vector<std::pair<double, uint16_t>> t;
+  if (t.empty()) {
+    for (uint32_t h = 0; h < 65536; ++h) {
+      const uint32_t e = (h >> 10) & 31u, m = h & 1023u;
+      if (e == 31) continue;  // inf / nan
+      double v = e == 0 ? std::ldexp((double)m, -24) : std::ldexp((double)(m | 1024u), (int)e - 25);
+      if (h & 0x8000u) v = -v;
+      t.push_back({v, (uint16_t)h});
+    }
+    std::sort(t.begin(), t.end(), [](const std::pair<double, uint16_t>& a, const std::pair<double, uint16_t>& b) {
+      return a.first < b.first || (a.first == b.first && a.second < b.second);
+    });
+  }
+  return t;
+}
+
+bool half_round(double x, bool up, uint16_t* out) {
+  const auto& t = half_table();
+  if (up) {  // smallest half >= x
+    auto it = std::lower_bound(t.begin(), t.end(), x, [](const std::pair<double, uint16_t>& a, double v) { return a.first < v; });
+    if (it == t.end()) return false;
+    *out = it->second;
+  } else {   // largest half <= x
+    auto it = std::upper_bound(t.begin(), t.end(), x, [](double v, const std::pair<double, uint16_t>& a) { return v < a.first; });
+    if (it == t.begin()) return false;
+    *out = (--it)->second;
+  }
+  return true;
+}
+
 int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_opts* opts,
                std::vector<uint8_t>& out) {
   if (!mesh) return set_error(CBVH_EINVAL, "mesh is null");
@@ -124,6 +157,9 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   int c = opts ? opts->leaf_size : 4;
   if (T < branching || T > (1 << 20)) return set_error(CBVH_EINVAL, "treelet_nodes must be >= branching");
   if (c < 1 || c > 4) return set_error(CBVH_EINVAL, "leaf_size must be in [1, 4]");
+  const int layout = opts ? opts->layout : CBVH_LAYOUT_DELTA;
+  if (layout != CBVH_LAYOUT_DELTA && layout != CBVH_LAYOUT_FP16 && layout != CBVH_LAYOUT_FP32)
+    return set_error(CBVH_EINVAL, "layout must be CBVH_LAYOUT_DELTA, _FP16 or _FP32");
   if (!mesh->vertices || !mesh->triangles) return set_error(CBVH_EINVAL, "null mesh arrays");
   const int64_t nv = mesh->num_vertices, nt = mesh->num_triangles;
   if (nt <= 0 || nv <= 0) return set_error(CBVH_EMESH, "empty mesh");
@@ -278,7 +314,8 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   }
 
   // ---- serialize
-  const uint32_t w = bits <= 4 ? 4 : bits <= 8 ? 8 : 16;
+  const uint32_t w = layout == CBVH_LAYOUT_FP32 ? 32u : layout == CBVH_LAYOUT_FP16 ? 16u
+                   : bits <= 4 ? 4u : bits <= 8 ? 8u : 16u;
   const size_t code_bytes_node = 6 * w / 8;
   size_t off_topo = 256;
   size_t off_codes = align256(off_topo + 4 * (size_t)n);
@@ -292,7 +329,7 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
     return set_error(CBVH_ENOMEM, "blob allocation failed");
   }
   std::memcpy(&out[0], "CBVH", 4);
-  put<uint32_t>(out, 4, 2u);
+  put<uint32_t>(out, 4, 3u);
   put<uint32_t>(out, 8, (uint32_t)branching);
   put<uint32_t>(out, 12, (uint32_t)bits);
   put<uint32_t>(out, 16, (uint32_t)T);
@@ -312,11 +349,28 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   put<uint64_t>(out, 112, off_tris);
   put<uint64_t>(out, 120, off_tri_index);
   put<uint64_t>(out, 128, total);
+  put<uint32_t>(out, 136, (uint32_t)layout);
   std::memcpy(&out[off_topo], topo.data(), 4 * (size_t)n);
   for (int nid = 0; nid < n; ++nid) {
     const uint16_t* q = &code[6 * (size_t)order[nid]];
     uint8_t* dst = &out[off_codes + code_bytes_node * nid];
-    if (w == 16) {
+    const BNode& nd = bd.nodes[order[nid]];
+    if (layout == CBVH_LAYOUT_FP32) {
+      // absolute boxes: min/max of fp32 coordinates are fp32 values (exact)
+      for (int a = 0; a < 3; ++a) {
+        put<float>(out, off_codes + code_bytes_node * nid + 4 * a, (float)nd.lo[a]);
+        put<float>(out, off_codes + code_bytes_node * nid + 12 + 4 * a, (float)nd.hi[a]);
+      }
+    } else if (layout == CBVH_LAYOUT_FP16) {
+      // binary16 (§III.A), rounded outward: lo down, hi up
+      for (int a = 0; a < 3; ++a) {
+        uint16_t hl, hh;
+        if (!half_round(nd.lo[a], false, &hl) || !half_round(nd.hi[a], true, &hh))
+          return set_error(CBVH_EMESH, "coordinate outside the binary16 range");
+        put<uint16_t>(out, off_codes + code_bytes_node * nid + 2 * a, hl);
+        put<uint16_t>(out, off_codes + code_bytes_node * nid + 6 + 2 * a, hh);
+      }
+    } else if (w == 16) {
       std::memcpy(dst, q, 12);
     } else if (w == 8) {
       for (int f = 0; f < 6; ++f) dst[f] = (uint8_t)q[f];
@@ -342,7 +396,9 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
   if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0) return set_error(CBVH_EBLOB, "bad magic");
   auto u32 = [&](size_t o) { uint32_t x; std::memcpy(&x, p + o, 4); return x; };
   auto u64 = [&](size_t o) { uint64_t x; std::memcpy(&x, p + o, 8); return x; };
-  if (u32(4) != 2) return set_error(CBVH_EBLOB, "unsupported blob version");
+  if (u32(4) != 3) return set_error(CBVH_EBLOB, "unsupported blob version");
+  h->layout = u32(136);
+  if (h->layout > 2) return set_error(CBVH_EBLOB, "bad layout");
   h->branching = u32(8); h->bits = u32(12); h->treelet_nodes = u32(16); h->leaf_size = u32(20);
   h->code_width = u32(24); h->num_nodes = u32(28); h->num_tris = u32(32); h->num_treelets = u32(36);
   h->depth = u32(40); h->num_leaves = u32(44);
@@ -354,7 +410,9 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
   if (h->total_bytes != bytes) return set_error(CBVH_EBLOB, "blob size does not match header");
   if (h->branching != 2 && h->branching != 4 && h->branching != 8) return set_error(CBVH_EBLOB, "bad branching");
   if (h->bits < 2 || h->bits > 16) return set_error(CBVH_EBLOB, "bad bits");
-  if (h->code_width != (h->bits <= 4 ? 4u : h->bits <= 8 ? 8u : 16u)) return set_error(CBVH_EBLOB, "bad code width");
+  const uint32_t want_w = h->layout == CBVH_LAYOUT_FP32 ? 32u : h->layout == CBVH_LAYOUT_FP16 ? 16u
+                        : h->bits <= 4 ? 4u : h->bits <= 8 ? 8u : 16u;
+  if (h->code_width != want_w) return set_error(CBVH_EBLOB, "bad code width");
   if (h->num_nodes == 0 || h->num_tris == 0 || h->num_nodes >= (1u << 28) || h->num_tris >= (1u << 29))
     return set_error(CBVH_EBLOB, "bad counts");
   const uint64_t cb = 6ull * h->code_width / 8;

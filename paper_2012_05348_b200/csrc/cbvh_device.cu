@@ -31,6 +31,7 @@
 // stack runs low.  Per-pose results are accumulated with warp-aggregated
 // atomics, so any warp may process any item.
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -58,7 +59,8 @@ struct DevTree {
   const float* tris;
   float ox, oy, oz, cell;
   float maxabs;      // max |coordinate| of the decoded root box (slack scale)
-  int bits, width;   // b and stored field width (4 / 8 / 16)
+  int bits, width;   // b and stored field width (4 / 8 / 16; 16 / 32 for the absolute layouts)
+  int layout;        // CBVH_LAYOUT_DELTA / _FP16 / _FP32
   uint32_t root_topo;
   int32_t root[6];   // decoded root lattice box
 };
@@ -185,6 +187,47 @@ __device__ __forceinline__ void to_float_box(const DevTree& T, const int32_t C[6
   hi[0] = __fmaf_ru(__int2float_rn(C[3]), T.cell, T.ox);
   hi[1] = __fmaf_ru(__int2float_rn(C[4]), T.cell, T.oy);
   hi[2] = __fmaf_ru(__int2float_rn(C[5]), T.cell, T.oz);
+}
+
+// ---------------------------------------------------------------- node boxes
+// A node's box travels as 6 words: lattice ints (DELTA) or fp32 bits
+// (FP16 / FP32, absolute).  The child box comes from the parent's words
+// (DELTA: predictor-corrector decode) or straight from the record.
+__device__ __forceinline__ void fetch_child_box(const DevTree& T, uint32_t node, const int32_t P[6], int32_t C[6]) {
+  if (T.layout == CBVH_LAYOUT_DELTA) {
+    uint32_t q[6];
+    load_codes(T, node, q);
+    decode_child(P, q, T.bits, C);
+  } else if (T.layout == CBVH_LAYOUT_FP16) {
+    // binary16 descriptors (§III.A): widened exactly to fp32
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(T.codes + 12ull * node);
+    const uint32_t a = __ldg(w), b = __ldg(w + 1), c = __ldg(w + 2);
+    const uint32_t h[6] = {a & 0xffffu, a >> 16, b & 0xffffu, b >> 16, c & 0xffffu, c >> 16};
+    #pragma unroll
+    for (int k = 0; k < 6; ++k) C[k] = __float_as_int(__half2float(__ushort_as_half((unsigned short)h[k])));
+  } else {
+    const float2* w = reinterpret_cast<const float2*>(T.codes + 24ull * node);
+    const float2 a = __ldg(w), b = __ldg(w + 1), c = __ldg(w + 2);
+    C[0] = __float_as_int(a.x); C[1] = __float_as_int(a.y); C[2] = __float_as_int(b.x);
+    C[3] = __float_as_int(b.y); C[4] = __float_as_int(c.x); C[5] = __float_as_int(c.y);
+  }
+}
+
+__device__ __forceinline__ void words_to_float(const DevTree& T, const int32_t C[6], float lo[3], float hi[3]) {
+  if (T.layout == CBVH_LAYOUT_DELTA) {
+    to_float_box(T, C, lo, hi);
+  } else {
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) { lo[k] = __int_as_float(C[k]); hi[k] = __int_as_float(C[3 + k]); }
+  }
+}
+
+// sum of the box's extents (the larger-first descent rule's size measure)
+__device__ __forceinline__ float words_extent(const DevTree& T, const int32_t C[6]) {
+  if (T.layout == CBVH_LAYOUT_DELTA)
+    return (float)((C[3] - C[0]) + (C[4] - C[1]) + (C[5] - C[2])) * T.cell;
+  return (__int_as_float(C[3]) - __int_as_float(C[0])) + (__int_as_float(C[4]) - __int_as_float(C[1])) +
+         (__int_as_float(C[5]) - __int_as_float(C[2]));
 }
 
 struct PoseF {
@@ -559,17 +602,10 @@ __device__ __forceinline__ int pair_count(uint32_t pw, uint32_t ta, uint32_t tb)
 // larger box (sum of extents, A-local vs world — rotation-invariant up to
 // sqrt 3), which visits the same leaf pairs (reading R15).
 __device__ __forceinline__ uint32_t descent_flags(int rule, uint32_t ta, uint32_t tb, const int32_t CA[6],
-                                                  const int32_t CB[6], float cellA, float cellB) {
+                                                  const int32_t CB[6], const DevTree& TA, const DevTree& TB) {
   const bool ai = !(ta & kLeafBit), bi = !(tb & kLeafBit);
   if (!(ai && bi) || rule == 0) return (ai ? kDescA : 0u) | (bi ? kDescB : 0u);
-#if CBVH_DESCENT_METRIC == 1
-  // max extent
-  const float ea = (float)max(CA[3] - CA[0], max(CA[4] - CA[1], CA[5] - CA[2])) * cellA;
-  const float eb = (float)max(CB[3] - CB[0], max(CB[4] - CB[1], CB[5] - CB[2])) * cellB;
-#else
-  const float ea = (float)((CA[3] - CA[0]) + (CA[4] - CA[1]) + (CA[5] - CA[2])) * cellA;
-  const float eb = (float)((CB[3] - CB[0]) + (CB[4] - CB[1]) + (CB[5] - CB[2])) * cellB;
-#endif
+  const float ea = words_extent(TA, CA), eb = words_extent(TB, CB);
   // similar sizes (within CBVH_DESCENT_BOTH): descend both, as Alg. 1 does
   if (ea < CBVH_DESCENT_BOTH * eb && eb < CBVH_DESCENT_BOTH * ea) return kDescA | kDescB;
   return ea >= eb ? kDescA : kDescB;
@@ -816,7 +852,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
               const int slot = top + c.lane;
               c.st[F_POSE * kStack + slot] =
                   (base + c.lane) | descent_flags(p.descent, p.A.root_topo, p.B.root_topo, p.A.root, p.B.root,
-                                                  p.A.cell, p.B.cell);
+                                                  p.A, p.B);
               c.st[F_TA * kStack + slot] = p.A.root_topo;
               c.st[F_TB * kStack + slot] = p.B.root_topo;
               #pragma unroll
@@ -944,27 +980,23 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
       if (valid) {
         if (a_int) {
           const uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
-          uint32_t q[6];
-          load_codes(p.A, node, q);
           cta = __ldg(p.A.topo + node);
-          decode_child(BA, q, p.A.bits, CA);
+          fetch_child_box(p.A, node, BA, CA);
         } else {
           #pragma unroll
           for (int r = 0; r < 6; ++r) CA[r] = BA[r];
         }
         if (b_int) {
           const uint32_t node = (tb & 0x0FFFFFFFu) + (uint32_t)j;
-          uint32_t q[6];
-          load_codes(p.B, node, q);
           ctb = __ldg(p.B.topo + node);
-          decode_child(BB, q, p.B.bits, CB);
+          fetch_child_box(p.B, node, BB, CB);
         } else {
           #pragma unroll
           for (int r = 0; r < 6; ++r) CB[r] = BB[r];
         }
         float alo[3], ahi[3], blo[3], bhi[3];
-        to_float_box(p.A, CA, alo, ahi);
-        to_float_box(p.B, CB, blo, bhi);
+        words_to_float(p.A, CA, alo, ahi);
+        words_to_float(p.B, CB, blo, bhi);
 #if CBVH_FILTER_TASKS
         #pragma unroll
         for (int k = 0; k < 3; ++k) { alo_s[k] = alo[k]; ahi_s[k] = ahi[k]; blo_s[k] = blo[k]; bhi_s[k] = bhi[k]; }
@@ -1038,7 +1070,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) 
         }
         if (push) {
           const int s2 = top + pos;
-          c.st[F_POSE * kStack + s2] = pose | descent_flags(p.descent, cta, ctb, CA, CB, p.A.cell, p.B.cell);
+          c.st[F_POSE * kStack + s2] = pose | descent_flags(p.descent, cta, ctb, CA, CB, p.A, p.B);
           c.st[F_TA * kStack + s2] = cta;
           c.st[F_TB * kStack + s2] = ctb;
           #pragma unroll
@@ -1226,6 +1258,7 @@ static DevTree make_tree(const cbvh_bvh* T) {
   d.cell = std::ldexp(1.0f, h.lattice_exp);
   d.bits = (int)h.bits;
   d.width = (int)h.code_width;
+  d.layout = (int)h.layout;
   return d;
 }
 
@@ -1316,6 +1349,26 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
   out->bytes = bytes;
   out->h = h;
   std::memcpy(&out->root_topo, h_blob + h.off_topo, 4);
+  if (h.layout != CBVH_LAYOUT_DELTA) {
+    // absolute layouts: the root's own stored box, as fp32 bit patterns
+    float m = 0.f;
+    for (int k = 0; k < 6; ++k) {
+      float v;
+      if (h.layout == CBVH_LAYOUT_FP32) {
+        std::memcpy(&v, h_blob + h.off_codes + 4 * k, 4);
+      } else {
+        uint16_t hv;
+        std::memcpy(&hv, h_blob + h.off_codes + 2 * k, 2);
+        const int e = (hv >> 10) & 31, mm = hv & 1023;
+        double d = e == 0 ? std::ldexp((double)mm, -24) : std::ldexp((double)(mm + 1024), e - 25);
+        v = (float)((hv & 0x8000) ? -d : d);
+      }
+      std::memcpy(&out->root_decoded[k], &v, 4);
+      m = std::fmax(m, std::fabs(v));
+    }
+    out->max_abs_coord = m;
+    return CBVH_OK;
+  }
   // node 0 is coded against the header root box (the anchor of treelet 0)
   uint32_t q[6];
   const uint8_t* c = h_blob + h.off_codes;

@@ -202,3 +202,68 @@ def test_error_paths():
         M.blob_info(ok.blob[:-16])
     info = L.cbvh_info()
     assert lib.cbvh_blob_info(None, 0, C.byref(info)) == L.CBVH_EINVAL
+
+
+# ------------------------------------------------------------------ node layouts (§III.A ablation)
+
+
+@pytest.mark.parametrize("layout", ["fp16", "fp32"])
+@pytest.mark.parametrize("B", [2, 4, 8])
+def test_absolute_layouts_invariants(cfg1, mesh16k, layout, B):
+    for m in (cfg1.A, mesh16k):
+        bv = M.build_compressed_bvh(m.vertices, m.triangles, B, 8, 32, 4, layout=layout)
+        r = O.check_blob(bv.blob, m.vertices, m.triangles)
+        assert r["violations"] == 0, r
+        assert bv.info["layout"] == layout
+        assert bv.info["code_bytes_per_node"] == (12 if layout == "fp16" else 24)  # Table I: 6 floats / halves
+
+
+def test_fp32_layout_is_exact(cfg1):
+    A = cfg1.A
+    bv = M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, 32, 4, layout="fp32")
+    dec = O.Tree.from_blob(bv.blob, A.vertices, A.triangles)
+    ex = O.Tree.from_blob(bv.blob, A.vertices, A.triangles, exact_boxes=True)
+    P = cfg1.poses[:16]
+    # exact boxes: identical BV-test counts under the verbatim Alg. 1 oracle
+    assert np.array_equal(O.collide(dec, dec, P, 0.0)[3], O.collide(ex, ex, P, 0.0)[3])
+
+
+def test_fp16_directed_rounding_spec_examples():
+    # 1.0 -> 0x3C00; 1.001 down -> 0x3C01 (1.0009765625), up -> 0x3C02
+    V = np.array([[1.001, 1.0, 0.0], [3.0, 1.001, 0.0], [2.0, 2.0, 1.0]], np.float32)
+    T = np.array([[0, 1, 2]], np.int32)
+    bv = M.build_compressed_bvh(V, T, 2, 8, 32, 4, layout="fp16")
+    off = bv.info["off_codes"]
+    h = np.frombuffer(bv.blob[off:off + 12].tobytes(), np.uint16)
+    lo, hi = h[:3], h[3:]
+    assert lo[0] == 0x3C01 and hi[0] == 0x4200   # x in [1.001, 3]
+    assert lo[1] == 0x3C00                         # y lo = 1.0 exactly
+    assert hi[1] == 0x4000 and hi[2] == 0x3C00     # y hi = 2, z hi = 1
+    Vu = np.array([[1.0, 1.001, 1.001], [0.5, 0.5, 0.5], [0.25, 0.25, 0.25]], np.float32)
+    bu = M.build_compressed_bvh(Vu, T, 2, 8, 32, 4, layout="fp16")
+    hu = np.frombuffer(bu.blob[bu.info["off_codes"] + 6:bu.info["off_codes"] + 12].tobytes(), np.uint16)
+    assert hu[1] == 0x3C02                         # 1.001 rounded up
+    assert O.check_blob(bu.blob, Vu, T)["violations"] == 0
+
+
+def test_fp16_range_error():
+    V = np.array([[0, 0, 0], [70000.0, 0, 0], [0, 1, 0]], np.float32)
+    T = np.array([[0, 1, 2]], np.int32)
+    with pytest.raises(L.CbvhError, match="EMESH"):
+        M.build_compressed_bvh(V, T, 2, 8, layout="fp16")
+    M.build_compressed_bvh(V, T, 2, 8, layout="fp32")
+
+
+def test_layout_cost_monotone_under_alg1(cfg1):
+    # S:419 / S:509: looser boxes cannot prune more (Alg. 1 verbatim oracle)
+    A, Bm, P = cfg1.A, cfg1.B, cfg1.poses[:32]
+    tests = {}
+    for lay in ("fp32", "fp16", "delta"):
+        ta = O.Tree.from_blob(M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, layout=lay).blob,
+                              A.vertices, A.triangles)
+        tb = O.Tree.from_blob(M.build_compressed_bvh(Bm.vertices, Bm.triangles, 4, 8, layout=lay).blob,
+                              Bm.vertices, Bm.triangles)
+        cnt, _, _, st = O.collide(ta, tb, P, 0.0)
+        tests[lay] = (st[0], cnt)
+    assert tests["fp16"][0] >= tests["fp32"][0] and tests["delta"][0] >= tests["fp32"][0]
+    assert np.array_equal(tests["fp16"][1], tests["fp32"][1]) and np.array_equal(tests["delta"][1], tests["fp32"][1])

@@ -53,8 +53,8 @@ def run_distance(M, A, B, poses, stats=False, descent="larger"):
     return out
 
 
-def build(M, mesh, B, bits, T=32):
-    return M.build_compressed_bvh(mesh.vertices, mesh.triangles, B, bits, T, 4).to_device()
+def build(M, mesh, B, bits, T=32, layout="delta"):
+    return M.build_compressed_bvh(mesh.vertices, mesh.triangles, B, bits, T, 4, layout=layout).to_device()
 
 
 def oracle_trees(w):
@@ -106,6 +106,21 @@ def test_config1_alg1_simultaneous_descent(M, cfg1, Bf):
     d64, _ = O.distance(tA, tB, w.poses[:128])
     check_distance(d1, d64, delta, "alg1 distance")
     check_distance(d2, d64, delta, "larger distance")
+
+
+@pytest.mark.parametrize("layout", ["fp16", "fp32"])
+def test_config1_absolute_layouts(M, cfg1, layout):
+    # binary16 / fp32 node boxes (the paper's §III.A comparison) through the
+    # same kernels: band rule vs the oracle, identical counts to the delta layout
+    w, tA, tB, delta, cnt, H, Z = cfg1
+    ref = run_collide(M, build(M, w.A, 4, 8), build(M, w.B, 4, 8), w.poses)
+    A, B = build(M, w.A, 4, 8, layout=layout), build(M, w.B, 4, 8, layout=layout)
+    hit, gc = run_collide(M, A, B, w.poses)
+    check_collide(hit, gc, H, Z, f"cfg1 {layout}")
+    assert np.array_equal(gc, ref[1])
+    d = run_distance(M, A, B, w.poses[:128])
+    d64, _ = O.distance(tA, tB, w.poses[:128])
+    check_distance(d, d64, delta, f"cfg1 distance {layout}")
 
 
 def test_config1_stats_variant_same_answer(M, cfg1):
@@ -256,6 +271,19 @@ def test_config4_distance_full_size_sampled(M):
     d64, _ = O.distance(tA, tB, w.poses[idx])
     rep = check_distance(d[idx], d64, O.band_delta(w.A.vertices), "cfg4")
     print("cfg4", rep)
+
+
+def test_config5_layouts_agree_full_size(M):
+    # full config 5 batch: fp16 / fp32 layouts count exactly what delta counts
+    w = G.make_config(5)
+    ref = None
+    for layout in ("delta", "fp16", "fp32"):
+        A = build(M, w.A, w.branching, w.bits, w.treelet, layout)
+        B = build(M, w.B, w.branching, w.bits, w.treelet, layout)
+        hit, gc = run_collide(M, A, B, w.poses)
+        if ref is None:
+            ref = gc
+        assert np.array_equal(gc, ref), layout
 
 
 def test_config5_full_size_sampled(M):
