@@ -418,7 +418,17 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
   #pragma unroll
   for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
   uint32_t m = 0;
-#if CBVH_FILTER_PIPE == 1
+#if CBVH_FILTER_PIPE == 2
+  // all records fetched up front, the (independent) tests fully unrolled
+  TriRec rec[4];
+  #pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (q < (int)cnt) rec[q] = load_rec(tris, first + q);
+  #pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q >= (int)cnt) break;
+    const Tri L = rec_tri(rec[q]);
+#elif CBVH_FILTER_PIPE == 1
   TriRec next = load_rec(tris, first);
   #pragma unroll 1
   for (uint32_t q = 0; q < cnt; ++q) {
@@ -447,6 +457,14 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
 
 #ifndef CBVH_LEAFPAIR_ONE_SIDE
 #define CBVH_LEAFPAIR_ONE_SIDE 0
+#endif
+#ifndef CBVH_DRAIN_INLINE
+#define CBVH_DRAIN_INLINE 1
+#endif
+#if CBVH_DRAIN_INLINE
+#define CBVH_DRAIN_ATTR __forceinline__
+#else
+#define CBVH_DRAIN_ATTR __noinline__
 #endif
 #ifndef CBVH_FILTER_TASKS
 #define CBVH_FILTER_TASKS 0
@@ -626,7 +644,7 @@ struct WarpCtx {
 // the c_A x c_B triangle pairs spread over the 32 lanes.  Returns the number
 // of triangle-pair tests (for stats).
 template <int MODE>
-__device__ __noinline__ unsigned drain_leaves(const Params& p, const WarpCtx c, int nleaf) {
+__device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx c, int nleaf) {
   unsigned tests = 0;
   int head = 0;
   while (head < nleaf) {
