@@ -85,8 +85,11 @@ static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte works
 #ifndef CBVH_DESCENT_METRIC
 #define CBVH_DESCENT_METRIC 0
 #endif
+#ifndef CBVH_MIN_BLOCKS_DIST
+#define CBVH_MIN_BLOCKS_DIST 2
+#endif
 #ifndef CBVH_MIN_BLOCKS
-#define CBVH_MIN_BLOCKS 4
+#define CBVH_MIN_BLOCKS 5
 #endif
 constexpr int kWarps = 4;           // warps per CTA
 #ifndef CBVH_STACK
@@ -815,7 +818,7 @@ __device__ __noinline__ bool dump_items(const Params& p, const WarpCtx c, int to
 }
 
 template <int MODE, bool STATS>
-__global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : 2) traverse_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBVH_MIN_BLOCKS_DIST) traverse_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint32_t smem[];
   const int wib = threadIdx.x >> 5;
   WarpCtx c;
