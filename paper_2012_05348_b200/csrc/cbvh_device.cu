@@ -86,7 +86,7 @@ static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte works
 #define CBVH_DESCENT_METRIC 0
 #endif
 #ifndef CBVH_MIN_BLOCKS_DIST
-#define CBVH_MIN_BLOCKS_DIST 2
+#define CBVH_MIN_BLOCKS_DIST 3
 #endif
 #ifndef CBVH_MIN_BLOCKS
 #define CBVH_MIN_BLOCKS 5
