@@ -232,7 +232,8 @@ def run(args):
         if distance:
             M.distance_batch(A, B, poses, dst, ws, stats=stats, descent=args.descent)
         else:
-            M.collide_batch(A, B, poses, hit, cnt, ws, stats=stats, descent=args.descent)
+            M.collide_batch(A, B, poses, hit, cnt, ws, stats=stats, descent=args.descent,
+                            early_exit=args.early_exit)
 
     # ---- warm-up (untimed)
     for _ in range(max(3, args.warmup)):
@@ -279,7 +280,7 @@ def run(args):
                               "dumped": st["dumped"], "launches": M.last_launch_count(),
                               "timeline_ms": [t / 1e6 for t in st["timeline_ns"]],
                               "lane_util": st["bv_tests"] / max(1, 32 * st["iterations"]),
-                              "iterations": st["iterations"], "bv_tests": st["bv_tests"], "layout": args.layout,
+                              "iterations": st["iterations"], "bv_tests": st["bv_tests"], "layout": args.layout, "early_exit": args.early_exit,
                               "bytes_per_node": {"A": A.info["bytes_per_node"], "B": B.info["bytes_per_node"]}}), flush=True)
         return
 
@@ -372,6 +373,8 @@ def main():
     ap.add_argument("--branching", type=int, default=0, help="override B (config-3 sweep)")
     ap.add_argument("--bits", type=int, default=0, help="override b (config-3 sweep)")
     ap.add_argument("--descent", default="larger", choices=["larger", "simultaneous"])
+    ap.add_argument("--early-exit", action="store_true",
+                    help="hit-only collide (stop each pose at its first hit); not the headline metric")
     ap.add_argument("--layout", default="delta", choices=["delta", "fp16", "fp32"],
                     help="node box layout (fp16/fp32: the paper's half-vs-float ablation)")
     ap.add_argument("--cpu-poses", type=int, default=100000)

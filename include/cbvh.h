@@ -160,8 +160,10 @@ enum {
   CBVH_DESCENT_SIMULTANEOUS = 0
 };
 typedef struct {
-  int descent; /* CBVH_DESCENT_* */
-  int stats;   /* non-zero: accumulate cbvh_stats in the workspace (slower) */
+  int descent;    /* CBVH_DESCENT_* */
+  int stats;      /* non-zero: accumulate cbvh_stats in the workspace (slower) */
+  int early_exit; /* collide only: stop each pose at its first colliding pair ("early_exit").
+                     d_hit stays exact; d_pair_count becomes a lower bound (>= 1 iff hit). */
 } cbvh_query_opts;
 
 /* collide_batch / distance_batch with options (opts may be null). */

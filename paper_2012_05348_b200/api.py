@@ -120,19 +120,21 @@ def _check_poses(poses):
     return int(poses.shape[0])
 
 
-def _opts(descent: str, stats: bool) -> L.cbvh_query_opts:
+def _opts(descent: str, stats: bool, early_exit: bool = False) -> L.cbvh_query_opts:
     if descent not in L.DESCENT:
         raise ValueError(f"descent must be one of {sorted(L.DESCENT)}")
-    return L.cbvh_query_opts(L.DESCENT[descent], 1 if stats else 0)
+    return L.cbvh_query_opts(L.DESCENT[descent], 1 if stats else 0, 1 if early_exit else 0)
 
 
 def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=None,
                   workspace: Workspace | None = None, stream=None, stats: bool = False,
-                  descent: str = "larger"):
+                  descent: str = "larger", early_exit: bool = False):
     """C-ABI collide_batch: per-pose hit flag (uint8) and colliding pair count (int32 view of uint32).
 
     descent: "larger" (default: descend the node with the larger box) or
-    "simultaneous" (Alg. 1 verbatim).  Both give identical results."""
+    "simultaneous" (Alg. 1 verbatim).  Both give identical results.
+    early_exit: stop each pose at its first hit (planning only needs the
+    boolean); the hit flag is exact, the count a lower bound."""
     torch = _torch()
     N = _check_poses(poses)
     dev = poses.device
@@ -142,7 +144,7 @@ def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=Non
         count = torch.empty(N, dtype=torch.int32, device=dev)
     if workspace is None:
         workspace = Workspace(A, B, 0, dev)
-    o = _opts(descent, stats)
+    o = _opts(descent, stats, early_exit)
     L.check(L.load().collide_batch_ex(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
                                       C.c_void_p(hit.data_ptr()), C.c_void_p(count.data_ptr()),
                                       C.c_void_p(workspace.ptr), workspace.nbytes,

@@ -128,6 +128,7 @@ struct Params {
   int nwarps;            // warps in the grid
   int budget;            // iterations a warp may run after its input is exhausted (< 0: unbounded)
   int descent;           // CBVH_DESCENT_SIMULTANEOUS (Alg. 1 verbatim) or CBVH_DESCENT_LARGER
+  int early_exit;        // collide: stop a pose's traversal at its first hit
 };
 
 // item pose word: bits 0..29 pose id, bit 30 = descend a, bit 31 = descend b
@@ -660,6 +661,8 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
       tb = c.lq[2 * kLeafQ + head + c.lane];
       mk = c.lq[3 * kLeafQ + head + c.lane];
       n = (int)((mk >> 8) & 7u) * (int)((mk >> 19) & 7u);  // only triangles the box filters kept
+      // early exit: a pose that already has a hit needs no more tests
+      if (MODE == 0 && p.early_exit && __ldcg(&p.hit[pose])) n = 0;
       // distance: a leaf pair whose box bound no longer beats the pose's best
       // distance (tightened since it was queued) is skipped
       if (MODE == 1 && __uint_as_float(c.lq[4 * kLeafQ + head + c.lane]) >= __uint_as_float(__ldcg(&p.dist_bits[pose])))
@@ -978,6 +981,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
     if (STATS) { s_exp += m; s_iter += passes; }
 
     const PoseF P = load_pose(p.poses, (int)pose);
+    const bool early_done = MODE == 0 && p.early_exit && __ldcg(&p.hit[pose]) != 0;
     const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
     const float eps = 2e-6f * (tmax + scale_ab);
     float best = FLT_MAX;
@@ -989,6 +993,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
       const int k = c.lane - start_e + 32 * pass;
       bool valid = (c.lane + 32 * pass) < total;
       if (MODE == 1) valid = valid && item_lb < best;
+      if (MODE == 0 && p.early_exit) valid = valid && !early_done;
       const int i = k / nb, j = k - i * nb;
       int32_t CA[6], CB[6];
       uint32_t cta = ta, ctb = tb;
@@ -1285,7 +1290,8 @@ static DevTree make_tree(const cbvh_bvh* T) {
 
 template <int MODE, bool STATS>
 static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
-                  uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream, int descent) {
+                  uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream, int descent,
+                  int early_exit) {
   g_launches = 0;
   if (!A || !B || !d_ws) return set_error(CBVH_EINVAL, "null argument");
   if (N < 0 || N > 0x3fffffffLL) return set_error(CBVH_EINVAL, "N out of range [0, 2^30)");
@@ -1321,6 +1327,7 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
   uint32_t* cont0 = p.spill + (size_t)s.warps * kSpillCap * kFields;
   uint32_t* cont1 = cont0 + (size_t)kContCap * kFields;
   p.descent = descent;
+  p.early_exit = (MODE == 0 && early_exit) ? 1 : 0;
   p.nwarps = s.warps;
   int ib = (int)((N + 255) / 256);
   ib = ib < 1 ? 1 : (ib > 4096 ? 4096 : ib);
@@ -1428,19 +1435,20 @@ size_t cbvh_workspace_bytes(const cbvh_bvh* A, const cbvh_bvh* B, int64_t N, int
 }
 
 static int opts_descent(const cbvh_query_opts* o) { return o ? o->descent : CBVH_DESCENT_LARGER; }
+static int opts_early(const cbvh_query_opts* o) { return o ? o->early_exit : 0; }
 static int opts_stats(const cbvh_query_opts* o) { return o ? o->stats : 0; }
 
 int collide_batch_ex(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                      uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream, const cbvh_query_opts* o) {
   if (opts_stats(o))
-    return launch<0, true>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o));
-  return launch<0, false>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o));
+    return launch<0, true>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o));
+  return launch<0, false>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o));
 }
 int distance_batch_ex(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, float* d_min_dist,
                       void* d_ws, size_t ws_bytes, void* stream, const cbvh_query_opts* o) {
   if (opts_stats(o))
-    return launch<1, true>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o));
-  return launch<1, false>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o));
+    return launch<1, true>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o));
+  return launch<1, false>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o));
 }
 int collide_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                   uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream) {
@@ -1448,7 +1456,7 @@ int collide_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
 }
 int collide_batch_stats(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                         uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream) {
-  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1};
+  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1, 0};
   return collide_batch_ex(A, B, d_poses, N, d_hit, d_pair_count, d_ws, ws_bytes, stream, &o);
 }
 int distance_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, float* d_min_dist,
@@ -1457,7 +1465,7 @@ int distance_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, i
 }
 int distance_batch_stats(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N,
                          float* d_min_dist, void* d_ws, size_t ws_bytes, void* stream) {
-  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1};
+  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1, 0};
   return distance_batch_ex(A, B, d_poses, N, d_min_dist, d_ws, ws_bytes, stream, &o);
 }
 

@@ -31,10 +31,10 @@ def M():
     return M
 
 
-def run_collide(M, A, B, poses, stats=False, descent="larger"):
+def run_collide(M, A, B, poses, stats=False, descent="larger", early_exit=False):
     P = torch.from_numpy(np.ascontiguousarray(poses)).cuda()
     ws = M.Workspace(A, B, 0)
-    hit, cnt = M.collide_batch(A, B, P, workspace=ws, stats=stats, descent=descent)
+    hit, cnt = M.collide_batch(A, B, P, workspace=ws, stats=stats, descent=descent, early_exit=early_exit)
     M.check(ws)
     out = hit.cpu().numpy(), cnt.cpu().numpy().view(np.uint32).astype(np.int64)
     if stats:
@@ -121,6 +121,19 @@ def test_config1_absolute_layouts(M, cfg1, layout):
     d = run_distance(M, A, B, w.poses[:128])
     d64, _ = O.distance(tA, tB, w.poses[:128])
     check_distance(d, d64, delta, f"cfg1 distance {layout}")
+
+
+def test_config1_early_exit(M, cfg1):
+    # early-exit hit flags equal the exhaustive ones; the count is a
+    # lower bound that is >= 1 exactly for colliding poses
+    w, tA, tB, delta, cnt, H, Z = cfg1
+    A, B = build(M, w.A, 2, 8), build(M, w.B, 2, 8)
+    h1, c1 = run_collide(M, A, B, w.poses)
+    h2, c2, st2 = run_collide(M, A, B, w.poses, stats=True, early_exit=True)
+    _, _, st1 = run_collide(M, A, B, w.poses, stats=True)
+    assert np.array_equal(h1, h2)
+    assert np.array_equal(c2 > 0, h2 == 1) and np.all(c2 <= c1)
+    assert st2["tri_tests"] < st1["tri_tests"]
 
 
 def test_config1_stats_variant_same_answer(M, cfg1):
@@ -284,6 +297,16 @@ def test_config5_layouts_agree_full_size(M):
         if ref is None:
             ref = gc
         assert np.array_equal(gc, ref), layout
+
+
+def test_config5_early_exit_full_size(M):
+    w = G.make_config(5)
+    A = build(M, w.A, w.branching, w.bits, w.treelet)
+    B = build(M, w.B, w.branching, w.bits, w.treelet)
+    h1, c1 = run_collide(M, A, B, w.poses)
+    h2, c2 = run_collide(M, A, B, w.poses, early_exit=True)
+    assert np.array_equal(h1, h2)
+    assert np.array_equal(c2 > 0, h2 == 1) and np.all(c2 <= c1)
 
 
 def test_config5_full_size_sampled(M):
