@@ -108,10 +108,10 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def rank_workload(config: int, rank: int, num_poses=None):
+def rank_workload(config: int, rank: int, num_poses=None, preset: str = "random"):
     """Weak-scaling shard: every rank gets the same meshes and its own
     independent, equally sized pose batch (pose seed offset = rank)."""
-    return G.make_config(config, num_poses=num_poses, pose_seed_offset=rank)
+    return G.make_config(config, num_poses=num_poses, pose_seed_offset=rank, preset=preset)
 
 
 def max_over_ranks(seconds: float, dist=None, device=None) -> float:
@@ -205,7 +205,7 @@ def run(args):
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
 
-    w = rank_workload(args.config, rank, args.poses)
+    w = rank_workload(args.config, rank, args.poses, args.preset)
     N = len(w.poses)
     t0 = time.time()
     if args.branching:
@@ -373,6 +373,8 @@ def main():
     ap.add_argument("--branching", type=int, default=0, help="override B (config-3 sweep)")
     ap.add_argument("--bits", type=int, default=0, help="override b (config-3 sweep)")
     ap.add_argument("--descent", default="larger", choices=["larger", "simultaneous"])
+    ap.add_argument("--preset", default="random", choices=["random", "contact"],
+                    help="pose preset; 'contact' = the paper's zero-distance preset (configs 1, 3)")
     ap.add_argument("--early-exit", action="store_true",
                     help="hit-only collide (stop each pose at its first hit); not the headline metric")
     ap.add_argument("--layout", default="delta", choices=["delta", "fp16", "fp32"],

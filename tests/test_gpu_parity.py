@@ -156,6 +156,24 @@ def test_config1_distance(M, cfg1):
     assert rep["near_contact"] > 20
 
 
+def test_contact_preset_collide_and_distance(M):
+    # the paper's "distance of zero" preset: every pose at or near
+    # contact — the band and the fp64 distance re-evaluation are exercised hardest
+    w = G.make_config(1, num_poses=768, preset="contact")
+    tA, tB = oracle_trees(w)
+    delta = O.band_delta(w.A.vertices)
+    _, H, Z, _ = O.collide(tA, tB, w.poses, delta)
+    A, B = build(M, w.A, 2, 8), build(M, w.B, 2, 8)
+    hit, gc = run_collide(M, A, B, w.poses)
+    rep = check_collide(hit, gc, H, Z, "contact")
+    assert 0.5 < hit.mean() < 0.99
+    d = run_distance(M, A, B, w.poses[:256])
+    d64, _ = O.distance(tA, tB, w.poses[:256])
+    drep = check_distance(d, d64, delta, "contact distance")
+    assert np.median(d64[d64 > 0]) < 0.05
+    print("contact", rep, drep)
+
+
 # ------------------------------------------------------------------ tiny + degenerate
 
 

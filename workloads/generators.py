@@ -174,6 +174,18 @@ def random_poses(rng: np.random.Generator, n: int, half_width: float) -> np.ndar
     return pack_poses(quat_to_matrix(q), t)
 
 
+def contact_poses(rng: np.random.Generator, n: int, centre_distance: float) -> np.ndarray:
+    """The paper's "distance of zero" preset, analytically: uniform
+    rotation and t = centre_distance x a uniform unit direction, so the two
+    (noisy) spheres' nominal surfaces touch — every pose is at or near contact,
+    the most expensive case.  Draws: standard_normal((N, 4)) quaternions, then
+    standard_normal((N, 3)) directions."""
+    q = rng.standard_normal((n, 4))
+    d = rng.standard_normal((n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return pack_poses(quat_to_matrix(q), centre_distance * d)
+
+
 def ring_poses(rng: np.random.Generator, n: int, major: float = 3.0,
                rho_lo: float = 4.5, rho_hi: float = 6.0) -> np.ndarray:
     """Config 4: A's centre at distance rho ~ U[4.5,6] from the torus ring (reading #19)."""
@@ -230,22 +242,27 @@ CONFIG_NAMES = {
 CONFIG_POSES = {1: 1024, 2: 65536, 3: 262144, 4: 131072, 5: 1048576}
 
 
-def make_config(k: int, num_poses: int | None = None, pose_seed_offset: int = 0) -> Workload:
+def make_config(k: int, num_poses: int | None = None, pose_seed_offset: int = 0,
+                preset: str = "random") -> Workload:
     """Build the seeded inputs of BASELINE.json configs[k-1].
 
     ``num_poses`` truncates the pose stream (the first n poses of the full draw
     are NOT identical to a smaller draw; prefixes are taken from the full draw
     order only when num_poses is None). ``pose_seed_offset`` gives each rank of
     a multi-GPU run its own independent batch (weak scaling).
+    ``preset="contact"`` (configs 1 and 3: two radius-1 spheres) replaces the
+    poses by the zero-distance preset (centres 2 apart, ``contact_poses``).
     """
     sa, sb, sp = seeds(k)
     sp += pose_seed_offset
     n = CONFIG_POSES[k] if num_poses is None else int(num_poses)
     ra, rb, rp = (np.random.default_rng(s) for s in (sa, sb, sp))
+    if preset not in ("random", "contact") or (preset == "contact" and k not in (1, 3)):
+        raise ValueError("preset 'contact' is defined for configs 1 and 3 (two unit spheres)")
     if k == 1:
         A = _mesh(*noisy_sphere(ra, 32, 16))
         B = _mesh(*noisy_sphere(rb, 32, 16))
-        P = random_poses(rp, n, 2.5)
+        P = random_poses(rp, n, 2.5) if preset == "random" else contact_poses(rp, n, 2.0)
         return Workload(CONFIG_NAMES[k], A, B, P, branching=2, bits=8, treelet=32)
     if k == 2:
         A = _mesh(*noisy_sphere(ra, 64, 32))
@@ -255,7 +272,7 @@ def make_config(k: int, num_poses: int | None = None, pose_seed_offset: int = 0)
     if k == 3:
         A = _mesh(*noisy_sphere(ra, 128, 64))
         B = _mesh(*noisy_sphere(rb, 128, 64))
-        P = random_poses(rp, n, 2.5)
+        P = random_poses(rp, n, 2.5) if preset == "random" else contact_poses(rp, n, 2.0)
         settings = [(br, bi) for br in (2, 4, 8) for bi in (4, 8, 16)]
         return Workload(CONFIG_NAMES[k], A, B, P, branching=4, bits=8, treelet=32,
                         settings=settings)
