@@ -682,7 +682,8 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
     const unsigned nz = __ballot_sync(FULL, c.lane < m && n > 0);
     const unsigned starts = __reduce_or_sync(FULL, (c.lane < m && n > 0) ? (1u << (incl - n)) : 0u);
     const int r = __popc(starts & ((2u << c.lane) - 1u)) - 1;
-    const int e = (nz != 0u && r >= 0) ? (int)__fns(nz, 0, r + 1) : 0;
+    // (collide never queues empty entries: the rank is the entry index)
+    const int e = MODE == 0 ? max(r, 0) : ((nz != 0u && r >= 0) ? (int)__fns(nz, 0, r + 1) : 0);
     const int start_e = __shfl_sync(FULL, incl - n, e);
     const uint32_t my_pose = __shfl_sync(FULL, pose, e);
     const uint32_t my_ta = __shfl_sync(FULL, ta, e);
