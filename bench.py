@@ -208,6 +208,8 @@ def run(args):
     w = rank_workload(args.config, rank, args.poses, args.preset)
     N = len(w.poses)
     t0 = time.time()
+    if args.leaf:
+        w.leaf = args.leaf
     if args.branching:
         w.branching = args.branching
     if args.bits:
@@ -371,6 +373,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
     ap.add_argument("--quick", action="store_true", help="timed steps only (A/B comparisons)")
     ap.add_argument("--branching", type=int, default=0, help="override B (config-3 sweep)")
+    ap.add_argument("--leaf", type=int, default=0, help="override the leaf size c (1..4)")
     ap.add_argument("--bits", type=int, default=0, help="override b (config-3 sweep)")
     ap.add_argument("--descent", default="larger", choices=["larger", "simultaneous"])
     ap.add_argument("--preset", default="random", choices=["random", "contact"],
