@@ -421,6 +421,23 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
   float c[3], h[3];
   #pragma unroll
   for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
+#if CBVH_FILTER_PRETEST
+  // the box as an oriented box in the triangles' own frame: centre oc,
+  // axes = columns of M, AABB radius orad (+ slack)
+  float oc[3], orad[3];
+  #pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    float acc = 0.f, rr = 0.f;
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float mk = DIR == 0 ? P.R[r][k] : P.R[k][r];
+      acc = fmaf(mk, DIR == 0 ? c[k] : c[k] - P.t[k], acc);
+      rr = fmaf(fabsf(mk), h[k], rr);
+    }
+    oc[r] = acc + (DIR == 0 ? P.t[r] : 0.f);
+    orad[r] = rr + eps;
+  }
+#endif
   uint32_t m = 0;
 #if CBVH_FILTER_PIPE == 2
   // all records fetched up front, the (independent) tests fully unrolled
@@ -443,6 +460,32 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
   #pragma unroll 1
   for (uint32_t q = 0; q < cnt; ++q) {
     const Tri L = rec_tri(load_rec(tris, first + q));
+#endif
+#if CBVH_FILTER_PRETEST
+    {
+      // cheap separating axes in the triangle's frame (no transform): its
+      // AABB vs the oriented box's AABB, and its stored normal (rec .c.yzw)
+      bool sep = false;
+      #pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float tlo = fminf(L.v[0][k], fminf(L.v[1][k], L.v[2][k]));
+        const float thi = fmaxf(L.v[0][k], fmaxf(L.v[1][k], L.v[2][k]));
+        sep = sep || tlo > oc[k] + orad[k] || thi < oc[k] - orad[k];
+      }
+      const float n0 = cur.c.y, n1 = cur.c.z, n2 = cur.c.w;
+      float rn = 0.f;
+      #pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        // n . (axis k of the box) = (R^T n)_k (DIR 0) or (R n)_k (DIR 1)
+        const float nk = DIR == 0 ? fmaf(n0, P.R[0][k], fmaf(n1, P.R[1][k], n2 * P.R[2][k]))
+                                  : fmaf(n0, P.R[k][0], fmaf(n1, P.R[k][1], n2 * P.R[k][2]));
+        rn = fmaf(fabsf(nk), h[k], rn);
+      }
+      const float sd = fmaf(n0, oc[0] - L.v[0][0], fmaf(n1, oc[1] - L.v[0][1], n2 * (oc[2] - L.v[0][2])));
+      const float nrm = fabsf(n0) + fabsf(n1) + fabsf(n2);
+      sep = sep || fabsf(sd) > fmaf(2.f * eps, nrm, rn);
+      if (sep) continue;
+    }
 #endif
     Tri W;
     if (DIR == 0) {
@@ -469,6 +512,9 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
 #define CBVH_DRAIN_ATTR __forceinline__
 #else
 #define CBVH_DRAIN_ATTR __noinline__
+#endif
+#ifndef CBVH_FILTER_PRETEST
+#define CBVH_FILTER_PRETEST 0
 #endif
 #ifndef CBVH_FILTER_TASKS
 #define CBVH_FILTER_TASKS 0
