@@ -44,7 +44,8 @@ enum {
   CBVH_ECUDA = -4,      /* a CUDA runtime call failed (message in cbvh_last_error) */
   CBVH_ENOMEM = -5,     /* host allocation failed */
   CBVH_EWORKSPACE = -6, /* workspace too small (see cbvh_workspace_bytes) */
-  CBVH_EOVERFLOW = -7   /* device traversal stack overflow (reported by cbvh_check) */
+  CBVH_EOVERFLOW = -7,  /* device traversal stack overflow (reported by cbvh_check) */
+  CBVH_EINTERNAL = -8   /* checked build only: a device bounds check failed (reported by cbvh_check) */
 };
 
 /* ------------------------------------------------------------------ build */

@@ -13,9 +13,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CBVH_LIB") or os.path.join(HERE, "libcbvh.so")
 
 CBVH_OK, CBVH_EINVAL, CBVH_EMESH, CBVH_EBLOB = 0, -1, -2, -3
-CBVH_ECUDA, CBVH_ENOMEM, CBVH_EWORKSPACE, CBVH_EOVERFLOW = -4, -5, -6, -7
+CBVH_ECUDA, CBVH_ENOMEM, CBVH_EWORKSPACE, CBVH_EOVERFLOW, CBVH_EINTERNAL = -4, -5, -6, -7, -8
 ERROR_NAMES = {0: "CBVH_OK", -1: "CBVH_EINVAL", -2: "CBVH_EMESH", -3: "CBVH_EBLOB", -4: "CBVH_ECUDA",
-               -5: "CBVH_ENOMEM", -6: "CBVH_EWORKSPACE", -7: "CBVH_EOVERFLOW"}
+               -5: "CBVH_ENOMEM", -6: "CBVH_EWORKSPACE", -7: "CBVH_EOVERFLOW", -8: "CBVH_EINTERNAL"}
 
 
 class cbvh_mesh(C.Structure):

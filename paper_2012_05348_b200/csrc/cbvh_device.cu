@@ -61,6 +61,7 @@ struct DevTree {
   float maxabs;      // max |coordinate| of the decoded root box (slack scale)
   int bits, width;   // b and stored field width (4 / 8 / 16; 16 / 32 for the absolute layouts)
   int layout;        // CBVH_LAYOUT_DELTA / _FP16 / _FP32
+  uint32_t n_nodes, n_tris;  // bounds for the checked build
   uint32_t root_topo;
   int32_t root[6];   // decoded root lattice box
 };
@@ -133,6 +134,18 @@ struct Params {
 
 // item pose word: bits 0..29 pose id, bit 30 = descend a, bit 31 = descend b
 constexpr uint32_t kPoseMask = 0x3FFFFFFFu;
+
+// Checked build (-DCBVH_CHECKED): device-side bounds checks of every node,
+// triangle, pose and queue index; a violation sets CBVH_EINTERNAL in the error
+// word (cbvh_check reports it).  compute-sanitizer is unavailable on the GPU
+// pool, so this is the memory-safety evidence (tests/test_gpu_checked.py).
+#ifdef CBVH_CHECKED
+#define CBVH_GUARD(p, cond, fix) \
+  do { if (!(cond)) { atomicExch(&(p).ctl->error, (unsigned)(-CBVH_EINTERNAL)); fix; } } while (0)
+#else
+#define CBVH_GUARD(p, cond, fix) do { } while (0)
+#endif
+#define CBVH_CHECK(p, cond) CBVH_GUARD(p, cond, (void)0)
 constexpr uint32_t kDescA = 0x40000000u;
 constexpr uint32_t kDescB = 0x80000000u;
 
@@ -805,6 +818,7 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
     const int ka = k / nb, kb = k - ka * nb;
     const uint32_t ia = (my_ta & 0x1FFFFFFFu) + ((my_mk >> (2 * ka)) & 3u);
     const uint32_t ib = (my_tb & 0x1FFFFFFFu) + ((my_mk >> (11 + 2 * kb)) & 3u);
+    CBVH_CHECK(p, !valid || (ia < p.A.n_tris && ib < p.B.n_tris && my_pose < (uint32_t)p.N));
     bool keep = false, hit = false;
     if (valid) {
       const PoseF P = load_pose(p.poses, (int)my_pose);
@@ -1108,6 +1122,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
     top -= m;
     if (STATS) { s_exp += m; s_iter += passes; }
 
+    CBVH_CHECK(p, pose < (uint32_t)p.N && slot >= 0 && slot < kStack);
     const PoseF P = load_pose(p.poses, (int)pose);
     const bool early_done = MODE == 0 && p.early_exit && __ldcg(&p.hit[pose]) != 0;
     const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
@@ -1133,7 +1148,8 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
 #endif
       if (valid) {
         if (a_int) {
-          const uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
+          uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
+          CBVH_GUARD(p, node < p.A.n_nodes, node = 0);
           cta = __ldg(p.A.topo + node);
           fetch_child_box(p.A, node, BA, CA);
         } else {
@@ -1141,7 +1157,8 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
           for (int r = 0; r < 6; ++r) CA[r] = BA[r];
         }
         if (b_int) {
-          const uint32_t node = (tb & 0x0FFFFFFFu) + (uint32_t)j;
+          uint32_t node = (tb & 0x0FFFFFFFu) + (uint32_t)j;
+          CBVH_GUARD(p, node < p.B.n_nodes, node = 0);
           ctb = __ldg(p.B.topo + node);
           fetch_child_box(p.B, node, BB, CB);
         } else {
@@ -1224,6 +1241,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
         }
         if (push) {
           const int s2 = top + pos;
+          CBVH_CHECK(p, s2 < kStack);
           c.st[F_POSE * kStack + s2] = pose | descent_flags(p.descent, cta, ctb, CA, CB, p.A, p.B);
           c.st[F_TA * kStack + s2] = cta;
           c.st[F_TB * kStack + s2] = ctb;
@@ -1241,6 +1259,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
       if (lm) {
         if (leafpair) {
           const int s2 = nleaf + __popc(lm & lt);
+          CBVH_CHECK(p, s2 < kLeafQ);
           c.lq[0 * kLeafQ + s2] = pose;
           c.lq[1 * kLeafQ + s2] = cta;
           c.lq[2 * kLeafQ + s2] = ctb;
@@ -1413,6 +1432,8 @@ static DevTree make_tree(const cbvh_bvh* T) {
   d.bits = (int)h.bits;
   d.width = (int)h.code_width;
   d.layout = (int)h.layout;
+  d.n_nodes = h.num_nodes;
+  d.n_tris = h.num_tris;
   return d;
 }
 
