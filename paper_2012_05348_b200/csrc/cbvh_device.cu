@@ -1143,13 +1143,14 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
       bool surv = false;
       float lb = 0.f;
       uint32_t mskA = 15u, mskB = 15u;
+      bool bad = false;  // checked build: an out-of-range child drops the lane
 #if CBVH_FILTER_TASKS
       float alo_s[3] = {0.f, 0.f, 0.f}, ahi_s[3] = {0.f, 0.f, 0.f}, blo_s[3] = {0.f, 0.f, 0.f}, bhi_s[3] = {0.f, 0.f, 0.f};
 #endif
       if (valid) {
         if (a_int) {
           uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
-          CBVH_GUARD(p, node < p.A.n_nodes, node = 0);
+          CBVH_GUARD(p, node < p.A.n_nodes, (node = 0, bad = true));
           cta = __ldg(p.A.topo + node);
           fetch_child_box(p.A, node, BA, CA);
         } else {
@@ -1158,7 +1159,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
         }
         if (b_int) {
           uint32_t node = (tb & 0x0FFFFFFFu) + (uint32_t)j;
-          CBVH_GUARD(p, node < p.B.n_nodes, node = 0);
+          CBVH_GUARD(p, node < p.B.n_nodes, (node = 0, bad = true));
           ctb = __ldg(p.B.topo + node);
           fetch_child_box(p.B, node, BB, CB);
         } else {
@@ -1210,6 +1211,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
           s_rec += (a_int ? 4 + 3 * p.A.width / 4 : 0) + (b_int ? 4 + 3 * p.B.width / 4 : 0);
         }
       }
+      if (bad) surv = false;
       if (STATS) s_bv += __popc(__ballot_sync(FULL, valid)) * (c.lane == 0 ? 1 : 0);
 #if CBVH_FILTER_TASKS
       if (MODE == 0) {
@@ -1522,6 +1524,27 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
   cbvh_header h;
   int rc = parse_header(h_blob, bytes, &h);
   if (rc) return rc;
+  // Topology validation (O(n)): children strictly after their parent (no
+  // cycles, guaranteed by the builder's treelet numbering) and inside the node
+  // array, leaf triangle ranges inside the soup — a corrupted blob must fail
+  // here, not loop or fault on the device.  (CBVH_SKIP_BLOB_VALIDATION=1 is a
+  // test hook for the checked build's device-side checks.)
+  const char* skip = std::getenv("CBVH_SKIP_BLOB_VALIDATION");
+  if (!(skip && skip[0] == '1')) {
+    const uint8_t* tp = h_blob + h.off_topo;
+    for (uint32_t n = 0; n < h.num_nodes; ++n) {
+      uint32_t w;
+      std::memcpy(&w, tp + 4ull * n, 4);
+      if (w & kLeafBit) {
+        const uint64_t first = w & 0x1FFFFFFFu, cnt = ((w >> 29) & 3u) + 1;
+        if (first + cnt > h.num_tris || cnt > h.leaf_size) return set_error(CBVH_EBLOB, "bad leaf triangle range");
+      } else {
+        const uint64_t first = w & 0x0FFFFFFFu, cnt = ((w >> 28) & 7u) + 1;
+        if (first <= n || first + cnt > h.num_nodes || cnt < 2 || cnt > h.branching)
+          return set_error(CBVH_EBLOB, "bad child range");
+      }
+    }
+  }
   out->d_blob = d_blob;
   out->bytes = bytes;
   out->h = h;

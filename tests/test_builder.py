@@ -267,3 +267,21 @@ def test_layout_cost_monotone_under_alg1(cfg1):
         tests[lay] = (st[0], cnt)
     assert tests["fp16"][0] >= tests["fp32"][0] and tests["delta"][0] >= tests["fp32"][0]
     assert np.array_equal(tests["fp16"][1], tests["fp32"][1]) and np.array_equal(tests["delta"][1], tests["fp32"][1])
+
+
+def test_bind_rejects_corrupt_topology(cfg1):
+    # cbvh_bind validates the topology on the host (no device allocation needed:
+    # bind only records the device pointer)
+    A = cfg1.A
+    bv = M.build_compressed_bvh(A.vertices, A.triangles, 2, 8)
+    lib = L.load()
+    out = L.cbvh_bvh()
+    fake_dev = C.c_void_p(1 << 20)  # 256-B aligned, never dereferenced by bind
+    ok = lib.cbvh_bind(bv.blob.ctypes.data_as(C.POINTER(C.c_uint8)), bv.blob.nbytes, fake_dev, C.byref(out))
+    assert ok == L.CBVH_OK
+    off = bv.info["off_topo"]
+    for bad_word in (0x0FFFFFF0, 0x00000000, 0x80000000 | 0x1FFFFFF0):  # far child / self-cycle / bad tris
+        b = bv.blob.copy()
+        b[off:off + 4] = np.frombuffer(np.uint32(bad_word).tobytes(), np.uint8)
+        rc = lib.cbvh_bind(b.ctypes.data_as(C.POINTER(C.c_uint8)), b.nbytes, fake_dev, C.byref(out))
+        assert rc == L.CBVH_EBLOB, hex(bad_word)

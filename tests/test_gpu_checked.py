@@ -4,8 +4,10 @@ and queue index on the device and reports a violation as CBVH_EINTERNAL.
 
 * the sanitizer case (configs 1 and 3, collide / early exit / stats /
   distance) runs clean under the checked build;
-* a blob whose root points past the node array is caught (the check clamps
-  the index, so the run itself stays in bounds).
+* a blob whose root points past the node array is caught on the device
+  (host validation bypassed; the offending lane is dropped, so the run stays
+  in bounds) — and by cbvh_bind's host validation otherwise
+  (tests/test_builder.py::test_bind_rejects_corrupt_topology).
 """
 import os
 import subprocess
@@ -18,8 +20,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CHECKED = os.path.join(ROOT, "paper_2012_05348_b200", "libcbvh_checked.so")
 
 
-def _run(code_or_file, *args, timeout=600):
-    env = dict(os.environ, CBVH_LIB=CHECKED)
+def _run(code_or_file, *args, timeout=300, extra_env=None):
+    env = dict(os.environ, CBVH_LIB=CHECKED, **(extra_env or {}))
     cmd = [sys.executable] + ([code_or_file] if code_or_file.endswith(".py") else ["-c", code_or_file]) + list(args)
     return subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
 
@@ -56,6 +58,7 @@ except L.CbvhError as e:
 
 
 def test_checked_build_catches_bad_index():
-    r = _run(CORRUPT)
+    # host validation bypassed so the device-side checks see the bad index
+    r = _run(CORRUPT, extra_env={"CBVH_SKIP_BLOB_VALIDATION": "1"})
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "CAUGHT -8" in r.stdout
