@@ -80,12 +80,6 @@ struct Control {
 };
 static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte workspace header");
 
-#ifndef CBVH_DESCENT_BOTH
-#define CBVH_DESCENT_BOTH 1.0f
-#endif
-#ifndef CBVH_DESCENT_METRIC
-#define CBVH_DESCENT_METRIC 0
-#endif
 #ifndef CBVH_MIN_BLOCKS_DIST
 #define CBVH_MIN_BLOCKS_DIST 3
 #endif
@@ -410,9 +404,6 @@ __device__ __forceinline__ Tri rec_tri(const TriRec& r) {
   return T;
 }
 
-#ifndef CBVH_FILTER_PIPE
-#define CBVH_FILTER_PIPE 1
-#endif
 
 // The box (centre c, half extents h) against the triangles of a leaf, each
 // mapped into the box's frame (DIR 0: B's world triangles into A's frame by
@@ -434,72 +425,13 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
   float c[3], h[3];
   #pragma unroll
   for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
-#if CBVH_FILTER_PRETEST
-  // the box as an oriented box in the triangles' own frame: centre oc,
-  // axes = columns of M, AABB radius orad (+ slack)
-  float oc[3], orad[3];
-  #pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    float acc = 0.f, rr = 0.f;
-    #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const float mk = DIR == 0 ? P.R[r][k] : P.R[k][r];
-      acc = fmaf(mk, DIR == 0 ? c[k] : c[k] - P.t[k], acc);
-      rr = fmaf(fabsf(mk), h[k], rr);
-    }
-    oc[r] = acc + (DIR == 0 ? P.t[r] : 0.f);
-    orad[r] = rr + eps;
-  }
-#endif
   uint32_t m = 0;
-#if CBVH_FILTER_PIPE == 2
-  // all records fetched up front, the (independent) tests fully unrolled
-  TriRec rec[4];
-  #pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (q < (int)cnt) rec[q] = load_rec(tris, first + q);
-  #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (q >= (int)cnt) break;
-    const Tri L = rec_tri(rec[q]);
-#elif CBVH_FILTER_PIPE == 1
   TriRec next = load_rec(tris, first);
   #pragma unroll 1
   for (uint32_t q = 0; q < cnt; ++q) {
     const TriRec cur = next;
     if (q + 1 < cnt) next = load_rec(tris, first + q + 1);
     const Tri L = rec_tri(cur);
-#else
-  #pragma unroll 1
-  for (uint32_t q = 0; q < cnt; ++q) {
-    const Tri L = rec_tri(load_rec(tris, first + q));
-#endif
-#if CBVH_FILTER_PRETEST
-    {
-      // cheap separating axes in the triangle's frame (no transform): its
-      // AABB vs the oriented box's AABB, and its stored normal (rec .c.yzw)
-      bool sep = false;
-      #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const float tlo = fminf(L.v[0][k], fminf(L.v[1][k], L.v[2][k]));
-        const float thi = fmaxf(L.v[0][k], fmaxf(L.v[1][k], L.v[2][k]));
-        sep = sep || tlo > oc[k] + orad[k] || thi < oc[k] - orad[k];
-      }
-      const float n0 = cur.c.y, n1 = cur.c.z, n2 = cur.c.w;
-      float rn = 0.f;
-      #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        // n . (axis k of the box) = (R^T n)_k (DIR 0) or (R n)_k (DIR 1)
-        const float nk = DIR == 0 ? fmaf(n0, P.R[0][k], fmaf(n1, P.R[1][k], n2 * P.R[2][k]))
-                                  : fmaf(n0, P.R[k][0], fmaf(n1, P.R[k][1], n2 * P.R[k][2]));
-        rn = fmaf(fabsf(nk), h[k], rn);
-      }
-      const float sd = fmaf(n0, oc[0] - L.v[0][0], fmaf(n1, oc[1] - L.v[0][1], n2 * (oc[2] - L.v[0][2])));
-      const float nrm = fabsf(n0) + fabsf(n1) + fabsf(n2);
-      sep = sep || fabsf(sd) > fmaf(2.f * eps, nrm, rn);
-      if (sep) continue;
-    }
-#endif
     Tri W;
     if (DIR == 0) {
       W = to_local(P, L);
@@ -515,9 +447,6 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
   return m;
 }
 
-#ifndef CBVH_LEAFPAIR_ONE_SIDE
-#define CBVH_LEAFPAIR_ONE_SIDE 0
-#endif
 #ifndef CBVH_DRAIN_INLINE
 #define CBVH_DRAIN_INLINE 1
 #endif
@@ -526,97 +455,6 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
 #else
 #define CBVH_DRAIN_ATTR __noinline__
 #endif
-#ifndef CBVH_FILTER_PRETEST
-#define CBVH_FILTER_PRETEST 0
-#endif
-#ifndef CBVH_FILTER_TASKS
-#define CBVH_FILTER_TASKS 0
-#endif
-#ifndef CBVH_TASKS_INLINE
-#define CBVH_TASKS_INLINE 1
-#endif
-#if CBVH_TASKS_INLINE
-#define CBVH_TASKS_ATTR __forceinline__
-#else
-#define CBVH_TASKS_ATTR __noinline__
-#endif
-
-// Warp-dense leaf refinement: every (surviving child pair, triangle of a leaf
-// side) test of the warp becomes one task; tasks are spread over the 32 lanes
-// in rounds (the per-lane loop left ~60 % of the lanes idle).  A lane needing
-// the B-side test (its A box vs B leaf ctb's triangles, in A's frame) owns
-// ntri(ctb) tasks, then ntri(cta) tasks for the A side (B box vs A leaf cta's
-// triangles, in the world).  Returns the refined survival; masks per side.
-__device__ CBVH_TASKS_ATTR bool leaf_filter_tasks(const Params& p, int lane, bool surv, uint32_t pose, uint32_t cta,
-                                               uint32_t ctb, const float alo[3], const float ahi[3],
-                                               const float blo[3], const float bhi[3], float eps,
-                                               uint32_t* mskA, uint32_t* mskB) {
-  const bool needB = surv && (ctb & kLeafBit), needA = surv && (cta & kLeafBit);
-  const int tB = needB ? (int)((ctb >> 29) & 3u) + 1 : 0;
-  const int tA = needA ? (int)((cta >> 29) & 3u) + 1 : 0;
-  const int t = tB + tA;
-  int incl = t;
-  #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(FULL, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const int off = incl - t;
-  const int total = __shfl_sync(FULL, incl, 31);
-  uint32_t bits = 0;
-  for (int r0 = 0; r0 < total; r0 += 32) {
-    // owner of task r0 + lane: lanes whose range starts in this round, or the
-    // one whose range runs into it from the previous round
-    const bool begins = t > 0 && off >= r0 && off < r0 + 32;
-    const unsigned bm = __ballot_sync(FULL, begins);
-    const unsigned starts = __reduce_or_sync(FULL, begins ? (1u << (off - r0)) : 0u);
-    const unsigned carry = __ballot_sync(FULL, t > 0 && off < r0 && off + t > r0);
-    const int nst = __popc(starts & ((2u << lane) - 1u));
-    const int owner = nst == 0 ? (carry ? __ffs(carry) - 1 : 0) : (int)__fns(bm, 0, nst);
-    const int o_off = __shfl_sync(FULL, off, owner);
-    const int o_tB = __shfl_sync(FULL, tB, owner);
-    const uint32_t o_pose = __shfl_sync(FULL, pose, owner);
-    const uint32_t o_leafB = __shfl_sync(FULL, ctb, owner), o_leafA = __shfl_sync(FULL, cta, owner);
-    const float o_eps = __shfl_sync(FULL, eps, owner);
-    const int j = r0 + lane - o_off;
-    const bool dir0 = j < o_tB;
-    float lo[3], hi[3];
-    #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const float a0 = __shfl_sync(FULL, alo[k], owner), a1 = __shfl_sync(FULL, ahi[k], owner);
-      const float b0 = __shfl_sync(FULL, blo[k], owner), b1 = __shfl_sync(FULL, bhi[k], owner);
-      lo[k] = dir0 ? a0 : b0;
-      hi[k] = dir0 ? a1 : b1;
-    }
-    bool ok = false;
-    if (r0 + lane < total) {
-      const PoseF P = load_pose(p.poses, (int)o_pose);
-      float cc[3], hh[3];
-      #pragma unroll
-      for (int k = 0; k < 3; ++k) { cc[k] = 0.5f * (lo[k] + hi[k]); hh[k] = 0.5f * (hi[k] - lo[k]); }
-      Tri W;
-      if (dir0) {
-        W = to_local(P, load_tri(p.B.tris, (o_leafB & 0x1FFFFFFFu) + (uint32_t)j));
-      } else {
-        const Tri L = load_tri(p.A.tris, (o_leafA & 0x1FFFFFFFu) + (uint32_t)(j - o_tB));
-        #pragma unroll
-        for (int v = 0; v < 3; ++v)
-          #pragma unroll
-          for (int k = 0; k < 3; ++k)
-            W.v[v][k] = fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], P.t[k])));
-      }
-      ok = box_tri_overlap(cc, hh, W, o_eps);
-    }
-    const unsigned rb = __ballot_sync(FULL, ok);
-    const int lo_i = max(off, r0), hi_i = min(off + t, r0 + 32);
-    if (t > 0 && lo_i < hi_i) bits |= ((rb >> (lo_i - r0)) & ((2u << (hi_i - lo_i - 1)) - 1u)) << (lo_i - off);
-  }
-  const uint32_t mb = bits & ((1u << tB) - 1u), ma = (bits >> tB) & ((1u << tA) - 1u);
-  *mskB = needB ? mb : 15u;
-  *mskA = needA ? ma : 15u;
-  return surv && (!needB || mb != 0u) && (!needA || ma != 0u);
-}
-
 // packed list of the set bits of a <= 4-bit mask: 2-bit indices, count
 __device__ __forceinline__ uint32_t pack_list(uint32_t m) {
   uint32_t list = 0, n = 0;
@@ -689,8 +527,6 @@ __device__ __forceinline__ uint32_t descent_flags(int rule, uint32_t ta, uint32_
   const bool ai = !(ta & kLeafBit), bi = !(tb & kLeafBit);
   if (!(ai && bi) || rule == 0) return (ai ? kDescA : 0u) | (bi ? kDescB : 0u);
   const float ea = words_extent(TA, CA), eb = words_extent(TB, CB);
-  // similar sizes (within CBVH_DESCENT_BOTH): descend both, as Alg. 1 does
-  if (ea < CBVH_DESCENT_BOTH * eb && eb < CBVH_DESCENT_BOTH * ea) return kDescA | kDescB;
   return ea >= eb ? kDescA : kDescB;
 }
 
@@ -1144,9 +980,6 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
       float lb = 0.f;
       uint32_t mskA = 15u, mskB = 15u;
       bool bad = false;  // checked build: an out-of-range child drops the lane
-#if CBVH_FILTER_TASKS
-      float alo_s[3] = {0.f, 0.f, 0.f}, ahi_s[3] = {0.f, 0.f, 0.f}, blo_s[3] = {0.f, 0.f, 0.f}, bhi_s[3] = {0.f, 0.f, 0.f};
-#endif
       if (valid) {
         if (a_int) {
           uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
@@ -1169,10 +1002,6 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
         float alo[3], ahi[3], blo[3], bhi[3];
         words_to_float(p.A, CA, alo, ahi);
         words_to_float(p.B, CB, blo, bhi);
-#if CBVH_FILTER_TASKS
-        #pragma unroll
-        for (int k = 0; k < 3; ++k) { alo_s[k] = alo[k]; ahi_s[k] = ahi[k]; blo_s[k] = blo[k]; bhi_s[k] = bhi[k]; }
-#endif
         if (MODE == 0) {
           surv = sat_gap<false>(P, alo, ahi, blo, bhi, eps, nullptr) <= 0.f;
           // Against a leaf, "intersect" is refined to the leaf's triangles
@@ -1181,18 +1010,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
           // box alone lets every A leaf crossing a B leaf box through.  For a
           // leaf pair both sides are filtered and the surviving triangles are
           // recorded as masks for the leaf phase.
-#if !CBVH_FILTER_TASKS
-#if CBVH_LEAFPAIR_ONE_SIDE
-          // a leaf pair refines only the larger leaf's side (the smaller
-          // leaf's few triangles rarely reject the larger box)
-          const bool lpair = (cta & kLeafBit) && (ctb & kLeafBit);
-          const float exa = (ahi[0] - alo[0]) + (ahi[1] - alo[1]) + (ahi[2] - alo[2]);
-          const float exb = (bhi[0] - blo[0]) + (bhi[1] - blo[1]) + (bhi[2] - blo[2]);
-          const bool doB = (ctb & kLeafBit) && (!lpair || exb >= exa);
-          const bool doA = (cta & kLeafBit) && (!lpair || exa > exb);
-#else
           const bool doB = (ctb & kLeafBit) != 0, doA = (cta & kLeafBit) != 0;
-#endif
           if (surv && doB) {
             mskB = box_hits_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps);
             surv = mskB != 0u;
@@ -1201,7 +1019,6 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
             mskA = box_hits_leaf<1>(P, blo, bhi, p.A.tris, cta, eps);
             surv = mskA != 0u;
           }
-#endif
         } else {
           sat_gap<true>(P, alo, ahi, blo, bhi, eps, &lb);
           surv = lb < best;
@@ -1213,14 +1030,6 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
       }
       if (bad) surv = false;
       if (STATS) s_bv += __popc(__ballot_sync(FULL, valid)) * (c.lane == 0 ? 1 : 0);
-#if CBVH_FILTER_TASKS
-      if (MODE == 0) {
-        uint32_t ma, mb;
-        surv = leaf_filter_tasks(p, c.lane, surv, pose, cta, ctb, alo_s, ahi_s, blo_s, bhi_s, eps, &ma, &mb);
-        mskA = ma;
-        mskB = mb;
-      }
-#endif
       const bool leafpair = surv && (cta & kLeafBit) && (ctb & kLeafBit);
       const bool push = surv && !leafpair;
       // ---- ballot/popc compaction: internal pairs back onto the stack
