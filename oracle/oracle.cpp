@@ -331,7 +331,7 @@ struct BlobView {
 template <class X> X rd(const uint8_t* p, size_t off) { X x; std::memcpy(&x, p + off, sizeof(X)); return x; }
 
 bool parse_blob(const uint8_t* p, size_t bytes, BlobView* b) {
-  if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0 || rd<uint32_t>(p, 4) != 3) return false;
+  if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0 || rd<uint32_t>(p, 4) != 4) return false;
   b->p = p; b->bytes = bytes;
   b->B = rd<uint32_t>(p, 8); b->bits = rd<uint32_t>(p, 12); b->T = rd<uint32_t>(p, 16);
   b->c = rd<uint32_t>(p, 20); b->w = rd<uint32_t>(p, 24); b->n_nodes = rd<uint32_t>(p, 28);
@@ -868,18 +868,27 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
         for (int v = 0; v < 3; ++v)
           for (int a = 0; a < 3; ++a)
             if (soup[12ull * s + 3 * v + a] != verts[3 * tris[3 * ti + v] + a]) report[4]++;
-        // stored normal: the fp64 cross product of the edges, rounded to fp32
-        {
-          double V[3][3];
-          for (int v = 0; v < 3; ++v)
-            for (int a = 0; a < 3; ++a) V[v][a] = (double)verts[3 * tris[3 * ti + v] + a];
-          double e1[3], e2[3], nn[3];
-          sub(V[1], V[0], e1); sub(V[2], V[0], e2); cross(e1, e2, nn);
-          double mag = std::sqrt(dot(nn, nn));
-          for (int a = 0; a < 3; ++a)
-            if (std::fabs((double)soup[12ull * s + 9 + a] - nn[a]) > 1e-6 * mag) report[4]++;
-        }
         subtree_tris[n].push_back(ti);
+      }
+      // leaf slab: record 0's pad = normal n, record 1's pad =
+      // (dmin, dmax); every vertex v of the leaf satisfies dmin <= n.v <= dmax
+      // (exactly, in fp64); other pads are zero
+      if (first < b.n_tris) {
+        double nn[3] = {(double)soup[12ull * first + 9], (double)soup[12ull * first + 10], (double)soup[12ull * first + 11]};
+        double lo = -INFINITY, hi = INFINITY;
+        if (cnt > 1) { lo = (double)soup[12ull * (first + 1) + 9]; hi = (double)soup[12ull * (first + 1) + 10]; }
+        if (std::fabs(std::sqrt(dot(nn, nn)) - 1.0) > 1e-6) report[4]++;
+        for (uint32_t k = 0; k < cnt && first + k < b.n_tris; ++k) {
+          for (int v = 0; v < 3; ++v) {
+            double x[3] = {(double)soup[12ull * (first + k) + 3 * v], (double)soup[12ull * (first + k) + 3 * v + 1],
+                           (double)soup[12ull * (first + k) + 3 * v + 2]};
+            double d = dot(nn, x);
+            if (cnt > 1 && (d < lo || d > hi)) report[1]++;
+          }
+          if (k >= 2 && (soup[12ull * (first + k) + 9] != 0.0f || soup[12ull * (first + k) + 10] != 0.0f ||
+                         soup[12ull * (first + k) + 11] != 0.0f)) report[4]++;
+          if (k == 1 && soup[12ull * (first + k) + 11] != 0.0f) report[4]++;
+        }
       }
     } else {
       uint32_t first = tp & 0x0FFFFFFFu, cnt = ((tp >> 28) & 7u) + 1;

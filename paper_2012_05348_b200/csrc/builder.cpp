@@ -19,6 +19,7 @@
 // The blob layout is DESIGN.md §3; the device side reads it in cbvh_device.cu.
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -285,12 +286,18 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
     if (nd.children.empty()) {
       ++leaves;
       uint32_t first = (uint32_t)tri_index.size(), cnt = (uint32_t)(nd.tri_end - nd.tri_begin);
+      // 48-byte records: v0 v1 v2 (xyz fp32) + 3 pad floats that carry the
+      // leaf's slab — a tighter bound of its triangles than its box (used by
+      // the device's box-vs-leaf test): record 0's pad = unit slab normal n
+      // (area-weighted mean of the triangle normals, fp32), record 1's pad =
+      // (dmin, dmax, 0) = the range of n.v over the leaf's vertices, computed
+      // in fp64 with the fp32 n and rounded outward (single-triangle leaves
+      // carry no range: the device takes it from the triangle's vertices).
+      double nsum[3] = {0, 0, 0};
+      std::vector<std::array<double, 3>> lv;
       for (int k = nd.tri_begin; k < nd.tri_end; ++k) {
         int t = bd.perm[k];
         tri_index.push_back((uint32_t)t);
-        // 48-byte record: v0 v1 v2 (xyz fp32) and n = (v1 - v0) x (v2 - v0)
-        // (computed in fp64 from the fp32 vertices, rounded once) — three
-        // 16-byte vectors; the normal serves the box-vs-triangle filters
         double w[3][3];
         for (int v = 0; v < 3; ++v)
           for (int a = 0; a < 3; ++a) {
@@ -298,11 +305,32 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
             soup.push_back(x);
             w[v][a] = (double)x;
           }
+        for (int z = 0; z < 3; ++z) soup.push_back(0.0f);
+        for (int v = 0; v < 3; ++v) lv.push_back({w[v][0], w[v][1], w[v][2]});
         double e1[3] = {w[1][0] - w[0][0], w[1][1] - w[0][1], w[1][2] - w[0][2]};
         double e2[3] = {w[2][0] - w[0][0], w[2][1] - w[0][1], w[2][2] - w[0][2]};
-        soup.push_back((float)(e1[1] * e2[2] - e1[2] * e2[1]));
-        soup.push_back((float)(e1[2] * e2[0] - e1[0] * e2[2]));
-        soup.push_back((float)(e1[0] * e2[1] - e1[1] * e2[0]));
+        nsum[0] += e1[1] * e2[2] - e1[2] * e2[1];
+        nsum[1] += e1[2] * e2[0] - e1[0] * e2[2];
+        nsum[2] += e1[0] * e2[1] - e1[1] * e2[0];
+      }
+      double len = std::sqrt(nsum[0] * nsum[0] + nsum[1] * nsum[1] + nsum[2] * nsum[2]);
+      float nf[3] = {0.f, 0.f, 1.f};
+      if (len > 0)
+        for (int a = 0; a < 3; ++a) nf[a] = (float)(nsum[a] / len);
+      double dmin = INFINITY, dmax = -INFINITY;
+      for (const auto& v : lv) {
+        const double d = (double)nf[0] * v[0] + (double)nf[1] * v[1] + (double)nf[2] * v[2];
+        dmin = std::min(dmin, d);
+        dmax = std::max(dmax, d);
+      }
+      float fmin_ = (float)dmin, fmax_ = (float)dmax;
+      if ((double)fmin_ > dmin) fmin_ = std::nextafter(fmin_, -INFINITY);
+      if ((double)fmax_ < dmax) fmax_ = std::nextafter(fmax_, INFINITY);
+      float* rec0 = &soup[12 * (size_t)first];
+      rec0[9] = nf[0]; rec0[10] = nf[1]; rec0[11] = nf[2];
+      if (cnt > 1) {
+        float* rec1 = &soup[12 * ((size_t)first + 1)];
+        rec1[9] = fmin_; rec1[10] = fmax_; rec1[11] = 0.0f;
       }
       topo[nid] = 0x80000000u | ((cnt - 1) << 29) | first;
     } else {
@@ -329,7 +357,7 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
     return set_error(CBVH_ENOMEM, "blob allocation failed");
   }
   std::memcpy(&out[0], "CBVH", 4);
-  put<uint32_t>(out, 4, 3u);
+  put<uint32_t>(out, 4, 4u);
   put<uint32_t>(out, 8, (uint32_t)branching);
   put<uint32_t>(out, 12, (uint32_t)bits);
   put<uint32_t>(out, 16, (uint32_t)T);
@@ -396,7 +424,7 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
   if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0) return set_error(CBVH_EBLOB, "bad magic");
   auto u32 = [&](size_t o) { uint32_t x; std::memcpy(&x, p + o, 4); return x; };
   auto u64 = [&](size_t o) { uint64_t x; std::memcpy(&x, p + o, 8); return x; };
-  if (u32(4) != 3) return set_error(CBVH_EBLOB, "unsupported blob version");
+  if (u32(4) != 4) return set_error(CBVH_EBLOB, "unsupported blob version");
   h->layout = u32(136);
   if (h->layout > 2) return set_error(CBVH_EBLOB, "bad layout");
   h->branching = u32(8); h->bits = u32(12); h->treelet_nodes = u32(16); h->leaf_size = u32(20);

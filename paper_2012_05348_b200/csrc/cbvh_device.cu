@@ -455,6 +455,61 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
 #else
 #define CBVH_DRAIN_ATTR __noinline__
 #endif
+#ifndef CBVH_LEAF_SLAB
+#define CBVH_LEAF_SLAB 0
+#endif
+
+// A box against the slab of a leaf (the range [dmin, dmax] of n.v over the
+// leaf's vertices, stored in the triangle records' pads — DESIGN.md §3): the
+// box, as an oriented box in the leaf's frame, is projected on n.
+// DIR 0: A's box (A-local) vs a B leaf (world): centre R c + t, radius sum_m |n.R_m| h_m
+// DIR 1: B's box (world) vs an A leaf (A-local): centre R^T (c - t), radius sum_k |(R n)_k| h_k
+template <int DIR>
+__device__ __forceinline__ bool box_vs_slab(const PoseF& P, const float lo[3], const float hi[3],
+                                            const float* tris, uint32_t leaf, float eps) {
+  const uint32_t first = leaf & 0x1FFFFFFFu, cnt = ((leaf >> 29) & 3u) + 1;
+  const float4* r0 = reinterpret_cast<const float4*>(tris + 12ull * first);
+  const float4 c0 = __ldg(r0 + 2);
+  const float n[3] = {c0.y, c0.z, c0.w};
+  float dlo, dhi;
+  if (cnt > 1) {
+    const float4 c1 = __ldg(reinterpret_cast<const float4*>(tris + 12ull * (first + 1)) + 2);
+    dlo = c1.y;
+    dhi = c1.z;
+  } else {
+    const float4 a0 = __ldg(r0), b0 = __ldg(r0 + 1);
+    const float d0 = fmaf(n[0], a0.x, fmaf(n[1], a0.y, n[2] * a0.z));
+    const float d1 = fmaf(n[0], a0.w, fmaf(n[1], b0.x, n[2] * b0.y));
+    const float d2 = fmaf(n[0], b0.z, fmaf(n[1], b0.w, n[2] * c0.x));
+    dlo = fminf(d0, fminf(d1, d2));
+    dhi = fmaxf(d0, fmaxf(d1, d2));
+  }
+  float cw[3], rad = 0.f;
+  #pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const float cr = 0.5f * (lo[r] + hi[r]), hr = 0.5f * (hi[r] - lo[r]);
+    // projection of the box's axis r on n
+    const float nr = DIR == 0 ? fmaf(n[0], P.R[0][r], fmaf(n[1], P.R[1][r], n[2] * P.R[2][r]))
+                              : fmaf(n[0], P.R[r][0], fmaf(n[1], P.R[r][1], n[2] * P.R[r][2]));
+    rad = fmaf(fabsf(nr), hr, rad);
+    cw[r] = cr;
+  }
+  float s;
+  if (DIR == 0) {
+    float x[3];
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) x[k] = fmaf(P.R[k][0], cw[0], fmaf(P.R[k][1], cw[1], fmaf(P.R[k][2], cw[2], P.t[k])));
+    s = fmaf(n[0], x[0], fmaf(n[1], x[1], n[2] * x[2]));
+  } else {
+    const float d0 = cw[0] - P.t[0], d1 = cw[1] - P.t[1], d2 = cw[2] - P.t[2];
+    float x[3];
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) x[k] = fmaf(P.R[0][k], d0, fmaf(P.R[1][k], d1, P.R[2][k] * d2));
+    s = fmaf(n[0], x[0], fmaf(n[1], x[1], n[2] * x[2]));
+  }
+  return s + rad + 2.f * eps >= dlo && s - rad - 2.f * eps <= dhi;
+}
+
 // packed list of the set bits of a <= 4-bit mask: 2-bit indices, count
 __device__ __forceinline__ uint32_t pack_list(uint32_t m) {
   uint32_t list = 0, n = 0;
@@ -1010,7 +1065,20 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
           // box alone lets every A leaf crossing a B leaf box through.  For a
           // leaf pair both sides are filtered and the surviving triangles are
           // recorded as masks for the leaf phase.
-          const bool doB = (ctb & kLeafBit) != 0, doA = (cta & kLeafBit) != 0;
+          const bool la = (cta & kLeafBit) != 0, lbf = (ctb & kLeafBit) != 0;
+#if CBVH_LEAF_SLAB
+          // an internal box against a leaf: the leaf's slab (one plane pair,
+          // DESIGN.md §4.2) — a leaf pair still refines per triangle (masks)
+          if (surv && lbf && !la) surv = box_vs_slab<0>(P, alo, ahi, p.B.tris, ctb, eps);
+          if (surv && la && !lbf) surv = box_vs_slab<1>(P, blo, bhi, p.A.tris, cta, eps);
+#if CBVH_LEAF_SLAB == 2
+          const bool doB = lbf, doA = la;
+#else
+          const bool doB = lbf && la, doA = la && lbf;
+#endif
+#else
+          const bool doB = lbf, doA = la;
+#endif
           if (surv && doB) {
             mskB = box_hits_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps);
             surv = mskB != 0u;

@@ -285,3 +285,20 @@ def test_bind_rejects_corrupt_topology(cfg1):
         b[off:off + 4] = np.frombuffer(np.uint32(bad_word).tobytes(), np.uint8)
         rc = lib.cbvh_bind(b.ctypes.data_as(C.POINTER(C.c_uint8)), b.nbytes, fake_dev, C.byref(out))
         assert rc == L.CBVH_EBLOB, hex(bad_word)
+
+
+def test_leaf_slab_containment_and_fault(cfg1):
+    # record pads carry each leaf's slab (unit n, [dmin, dmax] of n.v): the
+    # independent checker verifies containment; a shrunk range is caught
+    A = cfg1.A
+    bv = M.build_compressed_bvh(A.vertices, A.triangles, 4, 8)
+    assert O.check_blob(bv.blob, A.vertices, A.triangles)["violations"] == 0
+    info = bv.info
+    topo = np.frombuffer(bv.blob[info["off_topo"]:info["off_topo"] + 4 * info["num_nodes"]].tobytes(), np.uint32)
+    leaf = next(int(t) for t in topo if (t >> 31) and ((t >> 29) & 3) >= 1)  # a leaf with >= 2 triangles
+    first = leaf & 0x1FFFFFFF
+    rec1 = info["off_tris"] + 48 * (first + 1)
+    bad = bv.blob.copy()
+    dmin, dmax = np.frombuffer(bad[rec1 + 36:rec1 + 44].tobytes(), np.float32)
+    bad[rec1 + 40:rec1 + 44] = np.frombuffer(np.float32(dmin + 0.25 * (dmax - dmin)).tobytes(), np.uint8)
+    assert O.check_blob(bad, A.vertices, A.triangles)["containment"] > 0
