@@ -585,6 +585,13 @@ __device__ __forceinline__ uint32_t descent_flags(int rule, uint32_t ta, uint32_
   return ea >= eb ? kDescA : kDescB;
 }
 
+// floor(k / d) for 0 <= k < 2^12, 1 <= d <= 8 without an integer divide:
+// (k + 1/2) / d is at least 1/(2d) away from the next integer, far above the
+// ~1e-6 relative error of the fp32 reciprocal.
+__device__ __forceinline__ int small_div(int k, int d) {
+  return __float2int_rz(((float)k + 0.5f) * __frcp_rn((float)d));
+}
+
 // all triangles of a leaf: low (ntri) bits set
 __device__ __forceinline__ uint32_t full_mask(uint32_t t) { return (2u << ((t >> 29) & 3u)) - 1u; }
 
@@ -690,13 +697,23 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
     const unsigned fit = __ballot_sync(FULL, c.lane < avail && incl <= 32);
     const int m = __popc(fit);  // >= 2: an entry has at most 16 triangle pairs
     const int total = __shfl_sync(FULL, incl, m - 1);
-    // lane -> entry: rank among the non-empty entries (empty ones — distance
-    // pairs pruned above — share a start position with their successor)
-    const unsigned nz = __ballot_sync(FULL, c.lane < m && n > 0);
-    const unsigned starts = __reduce_or_sync(FULL, (c.lane < m && n > 0) ? (1u << (incl - n)) : 0u);
-    const int r = __popc(starts & ((2u << c.lane) - 1u)) - 1;
-    // (collide never queues empty entries unless it exits early)
-    const int e = (MODE == 0 && !p.early_exit) ? max(r, 0) : ((nz != 0u && r >= 0) ? (int)__fns(nz, 0, r + 1) : 0);
+    // lane -> entry: rank among the non-empty entries.  Empty entries (pruned
+    // distance pairs, early-exit poses) share a start position with their
+    // successor, so the non-empty ones are first compacted (in registers of
+    // the lanes: entry of rank r moves to lane r) — a shuffle, not __fns.
+    const bool nonempty = c.lane < m && n > 0;
+    const unsigned nz = __ballot_sync(FULL, nonempty);
+    const unsigned starts = __reduce_or_sync(FULL, nonempty ? (1u << (incl - n)) : 0u);
+    const int r = max(__popc(starts & ((2u << c.lane) - 1u)) - 1, 0);
+    int e = r;
+    if ((nz & (nz + 1u)) != 0u) {  // the non-empty entries are not a prefix
+      // lane r needs the index of the r-th non-empty entry: scatter it
+      // through the entries' lower-bound slots (already read this round)
+      if (nonempty) c.lq[4 * kLeafQ + head + __popc(nz & lt)] = (uint32_t)c.lane;
+      __syncwarp();
+      e = (int)c.lq[4 * kLeafQ + head + min(r, __popc(nz) - 1)];
+      __syncwarp();
+    }
     const int start_e = __shfl_sync(FULL, incl - n, e);
     const uint32_t my_pose = __shfl_sync(FULL, pose, e);
     const uint32_t my_ta = __shfl_sync(FULL, ta, e);
@@ -706,7 +723,7 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
     const int k = c.lane - start_e;
     // my_mk: bits 0-7 / 11-18 packed 2-bit triangle lists of A / B, counts at 8 / 19
     const int nb = max(1, (int)((my_mk >> 19) & 7u));
-    const int ka = k / nb, kb = k - ka * nb;
+    const int ka = small_div(k, nb), kb = k - ka * nb;
     const uint32_t ia = (my_ta & 0x1FFFFFFFu) + ((my_mk >> (2 * ka)) & 3u);
     const uint32_t ib = (my_tb & 0x1FFFFFFFu) + ((my_mk >> (11 + 2 * kb)) & 3u);
     CBVH_CHECK(p, !valid || (ia < p.A.n_tris && ib < p.B.n_tris && my_pose < (uint32_t)p.N));
@@ -1028,7 +1045,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
       bool valid = (c.lane + 32 * pass) < total;
       if (MODE == 1) valid = valid && item_lb < best;
       if (MODE == 0 && p.early_exit) valid = valid && !early_done;
-      const int i = k / nb, j = k - i * nb;
+      const int i = small_div(k, nb), j = k - i * nb;
       int32_t CA[6], CB[6];
       uint32_t cta = ta, ctb = tb;
       bool surv = false;
