@@ -83,6 +83,10 @@ __device__ __noinline__ bool coplanar2(const F* N, const TriT<F>& V, const TriT<
   return pt_in_tri2(v[0], u[0], u[1], u[2]) || pt_in_tri2(u[0], v[0], v[1], v[2]);
 }
 
+// (div_ is the fast fp32 division in the float instantiation: every
+// parameter it produces is clamped / tested, so a candidate is always a real
+// point pair and rounding can only over-estimate a distance.)
+
 // Möller 1997: the interval a triangle cuts on the line of the two planes,
 // from the projections p[] of its vertices and their plane distances d[]
 // (k = the vertex alone on its side).
@@ -133,7 +137,7 @@ __device__ __forceinline__ F pt_seg_d2(const F* p, const F* a, const F* b) {
   F ab[3], ap[3];
   vsub(b, a, ab); vsub(p, a, ap);
   F L = vdot(ab, ab);
-  F t = L > 0 ? clamp01(vdot(ap, ab) / L) : F(0);
+  F t = L > 0 ? clamp01(div_(vdot(ap, ab), L)) : F(0);
   F q[3] = {fma_(t, ab[0], a[0]) - p[0], fma_(t, ab[1], a[1]) - p[1], fma_(t, ab[2], a[2]) - p[2]};
   return vdot(q, q);
 }
@@ -149,7 +153,8 @@ __device__ F seg_seg_d2(const F* p0, const F* p1, const F* q0, const F* q1) {
   F a = vdot(d1, d1), e = vdot(d2, d2), b = vdot(d1, d2), c = vdot(d1, r), f = vdot(d2, r);
   F den = a * e - b * b;
   if (den > 0) {
-    F s = (b * f - c * e) / den, t = (a * f - b * c) / den;
+    const F inv = div_(F(1), den);
+    F s = (b * f - c * e) * inv, t = (a * f - b * c) * inv;
     if (s >= 0 && s <= 1 && t >= 0 && t <= 1) {
       F w[3] = {r[0] + s * d1[0] - t * d2[0], r[1] + s * d1[1] - t * d2[1], r[2] + s * d1[2] - t * d2[2]};
       best = fmin(best, vdot(w, w));
@@ -168,7 +173,7 @@ __device__ F pt_tri_d2(const F* p, const TriT<F>& T) {
   F nn = vdot(n, n);
   if (nn > 0) {
     vsub(p, T.v[0], w);
-    F h = vdot(w, n) / nn;
+    F h = div_(vdot(w, n), nn);
     F q[3] = {p[0] - h * n[0], p[1] - h * n[1], p[2] - h * n[2]};
     F a[3], b[3], c0[3];
     vsub(T.v[1], T.v[0], a); vsub(q, T.v[0], b); vcross(a, b, c0);
