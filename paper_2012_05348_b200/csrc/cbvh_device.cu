@@ -455,6 +455,9 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
 #else
 #define CBVH_DRAIN_ATTR __noinline__
 #endif
+#ifndef CBVH_DIST_DRAIN
+#define CBVH_DIST_DRAIN 2   // distance: drain the leaf queue once it holds this many pairs
+#endif
 #ifndef CBVH_LEAF_SLAB
 #define CBVH_LEAF_SLAB 0
 #endif
@@ -1171,7 +1174,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
       __syncwarp();
       // collide: drain in full rounds; distance: drain promptly so that the
       // pose's best distance tightens and prunes the rest of the traversal
-      if (nleaf > kLeafQ - 32 || (MODE == 1 && nleaf >= 2)) {
+      if (nleaf > kLeafQ - 32 || (MODE == 1 && nleaf >= CBVH_DIST_DRAIN)) {
         s_tri += drain_leaves<MODE>(p, c, nleaf);
         nleaf = 0;
       }
