@@ -120,6 +120,20 @@ def _check_poses(poses):
     return int(poses.shape[0])
 
 
+def validate_poses(poses, tol: float = 1e-6) -> np.ndarray:
+    """Host-side pose check (R orthonormal within 1e-6; finite values).
+
+    Returns the indices of the poses that fail.  Optional and never done on
+    the device; the kernels accept any finite [R|t] and apply R^T
+    as the inverse rotation.  Accepts a numpy array or a tensor [N, 12]."""
+    P = poses.detach().cpu().numpy() if hasattr(poses, "detach") else np.asarray(poses)
+    P = np.asarray(P, dtype=np.float64).reshape(-1, 12)
+    R = P[:, [0, 1, 2, 4, 5, 6, 8, 9, 10]].reshape(-1, 3, 3)
+    err = np.abs(np.einsum("nij,nkj->nik", R, R) - np.eye(3)).max(axis=(1, 2))
+    bad = ~np.isfinite(P).all(axis=1) | ~(err <= tol) | (np.linalg.det(R) <= 0)
+    return np.nonzero(bad)[0]
+
+
 def _opts(descent: str, stats: bool, early_exit: bool = False) -> L.cbvh_query_opts:
     if descent not in L.DESCENT:
         raise ValueError(f"descent must be one of {sorted(L.DESCENT)}")

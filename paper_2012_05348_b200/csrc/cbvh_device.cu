@@ -86,7 +86,10 @@ static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte works
 #ifndef CBVH_MIN_BLOCKS
 #define CBVH_MIN_BLOCKS 5
 #endif
-constexpr int kWarps = 4;           // warps per CTA
+#ifndef CBVH_WARPS
+#define CBVH_WARPS 4
+#endif
+constexpr int kWarps = CBVH_WARPS;  // warps per CTA
 #ifndef CBVH_STACK
 #define CBVH_STACK 96
 #endif

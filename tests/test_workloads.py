@@ -48,3 +48,13 @@ def test_determinism_and_rank_offsets():
     c = G.make_config(2, num_poses=128, pose_seed_offset=1)
     assert np.array_equal(a.poses, b.poses) and np.array_equal(a.B.vertices, b.B.vertices)
     assert not np.array_equal(a.poses, c.poses) and np.array_equal(a.B.vertices, c.B.vertices)
+
+
+def test_validate_poses():
+    import paper_2012_05348_b200 as M
+    P = G.make_config(1, num_poses=64).poses.copy()
+    assert len(M.validate_poses(P)) == 0
+    P[3, 0] *= 1.01          # not orthonormal
+    P[7, 5] = np.nan          # not finite
+    P[9, [0, 5, 10]] = [-1, -1, -1]   # reflection (det = -1)
+    assert list(M.validate_poses(P)) == [3, 7, 9]
