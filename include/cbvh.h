@@ -67,6 +67,8 @@ typedef struct {
   int treelet_nodes; /* T: nodes per treelet ("clustering BVHs into smaller parts"); default 32; must be >= branching */
   int leaf_size;     /* c: max triangles per leaf, 1..4; default 4 */
   int layout;        /* CBVH_LAYOUT_*; default CBVH_LAYOUT_DELTA (bits is ignored for FP16 / FP32) */
+  int kdop;          /* k of the k-DOP bounding volumes (Table I): 0 or 6 = AABB (default), 14, 18, 26;
+                        k > 6 requires CBVH_LAYOUT_DELTA and is supported for the static model B */
 } cbvh_build_opts;
 
 /* Build the compressed BVH of one mesh ("splitting the models and wrap it
@@ -96,6 +98,8 @@ typedef struct {
   int32_t root_box[6]; /* lattice lo xyz, hi xyz of the root */
   uint64_t off_topo, off_codes, off_treelets, off_tris, off_tri_index, total_bytes;
   uint32_t layout;     /* CBVH_LAYOUT_* */
+  uint32_t kdop;       /* 6 (AABB) or 14 / 18 / 26 */
+  uint64_t off_axes;   /* k-DOP axis table: per extra axis {fp32 origin, int32 exp, int32 root lo, root hi} */
 } cbvh_header;
 
 typedef struct {
@@ -103,7 +107,7 @@ typedef struct {
   uint64_t bvh_bytes;      /* topo + codes + treelet table: the compressed hierarchy */
   uint64_t tri_bytes;      /* leaf-ordered fp32 triangle soup (48 B / triangle: 9 floats + 3 pads) */
   double bytes_per_node;   /* bvh_bytes / num_nodes */
-  double code_bytes_per_node; /* the BV descriptor alone: 6 * code_width / 8 (3 / 6 / 12 delta, 12 fp16, 24 fp32) */
+  double code_bytes_per_node; /* the BV descriptor alone: k * code_width / 8 (AABB: 3 / 6 / 12 delta, 12 fp16, 24 fp32) */
 } cbvh_info;
 
 /* Validate and describe a host blob.  Errors: CBVH_EINVAL (null), CBVH_EBLOB. */

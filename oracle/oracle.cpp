@@ -326,12 +326,15 @@ struct BlobView {
   int32_t root[6];
   uint64_t off_topo, off_codes, off_treelets, off_tris, off_tri_index, total;
   uint32_t layout;  // 0 delta (lattice corrections), 1 absolute binary16, 2 absolute fp32
+  uint32_t kdop;    // 6 (AABB) or 14 / 18 / 26: k/2 slab axes per node
+  uint64_t off_axes;
+  uint32_t nax() const { return kdop / 2; }
 };
 
 template <class X> X rd(const uint8_t* p, size_t off) { X x; std::memcpy(&x, p + off, sizeof(X)); return x; }
 
 bool parse_blob(const uint8_t* p, size_t bytes, BlobView* b) {
-  if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0 || rd<uint32_t>(p, 4) != 4) return false;
+  if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0 || rd<uint32_t>(p, 4) != 5) return false;
   b->p = p; b->bytes = bytes;
   b->B = rd<uint32_t>(p, 8); b->bits = rd<uint32_t>(p, 12); b->T = rd<uint32_t>(p, 16);
   b->c = rd<uint32_t>(p, 20); b->w = rd<uint32_t>(p, 24); b->n_nodes = rd<uint32_t>(p, 28);
@@ -342,6 +345,9 @@ bool parse_blob(const uint8_t* p, size_t bytes, BlobView* b) {
   b->off_topo = rd<uint64_t>(p, 88); b->off_codes = rd<uint64_t>(p, 96); b->off_treelets = rd<uint64_t>(p, 104);
   b->off_tris = rd<uint64_t>(p, 112); b->off_tri_index = rd<uint64_t>(p, 120); b->total = rd<uint64_t>(p, 128);
   b->layout = rd<uint32_t>(p, 136);
+  b->kdop = rd<uint32_t>(p, 140);
+  b->off_axes = rd<uint64_t>(p, 144);
+  if (b->kdop != 6 && b->kdop != 14 && b->kdop != 18 && b->kdop != 26) return false;
   if (b->total != bytes) return false;
   if (b->layout == 0 && b->w != 4 && b->w != 8 && b->w != 16) return false;
   if (b->layout == 1 && b->w != 16) return false;
@@ -376,14 +382,21 @@ void abs_box(const BlobView& b, uint32_t n, double* lo, double* hi) {
 uint32_t blob_topo(const BlobView& b, uint32_t n) { return rd<uint32_t>(b.p, b.off_topo + 4ull * n); }
 
 // The six stored corrections of node n: order lo_x, lo_y, lo_z, hi_x, hi_y, hi_z.
+// Stored field f of node n (fields: lo of the k/2 axes, then hi of the k/2
+// axes; axes 0-2 are x, y, z): w-bit unsigned, little-endian, 4-bit fields
+// packed two per byte (low nibble first).
+uint32_t code_field(const BlobView& b, uint32_t n, uint32_t f) {
+  const uint64_t base = b.off_codes + (uint64_t)n * (2ull * b.nax() * b.w / 8);
+  if (b.w == 16) return rd<uint16_t>(b.p, base + 2 * f);
+  if (b.w == 8) return b.p[base + f];
+  return (b.p[base + f / 2] >> (4 * (f % 2))) & 15u;
+}
+
+// The box corrections of node n: lo_x, lo_y, lo_z, hi_x, hi_y, hi_z.
 void blob_codes(const BlobView& b, uint32_t n, uint32_t q[6]) {
-  if (b.w == 16) {
-    for (int f = 0; f < 6; ++f) q[f] = rd<uint16_t>(b.p, b.off_codes + 12ull * n + 2 * f);
-  } else if (b.w == 8) {
-    for (int f = 0; f < 6; ++f) q[f] = b.p[b.off_codes + 6ull * n + f];
-  } else {
-    uint32_t word = b.p[b.off_codes + 3ull * n] | (b.p[b.off_codes + 3ull * n + 1] << 8) | (b.p[b.off_codes + 3ull * n + 2] << 16);
-    for (int f = 0; f < 6; ++f) q[f] = (word >> (4 * f)) & 15u;
+  for (int a = 0; a < 3; ++a) {
+    q[a] = code_field(b, n, a);
+    q[3 + a] = code_field(b, n, b.nax() + a);
   }
 }
 
@@ -969,6 +982,58 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
     }
   }
   if (expect_first != b.n_nodes) report[5]++;
+  // k-DOP slab axes (layout 0 only): decode every extra axis top-down (DFS
+  // preorder has parents first), then check child-in-parent and containment of
+  // the exact projections of each subtree's vertices (bottom-up).
+  if (b.layout == 0 && b.kdop > 6) {
+    static const int dirs[10][3] = {{1, 1, 1}, {1, 1, -1}, {1, -1, 1}, {-1, 1, 1}, {1, 1, 0},
+                                    {1, -1, 0}, {1, 0, 1}, {1, 0, -1}, {0, 1, 1}, {0, 1, -1}};
+    const int nx = (int)b.nax() - 3;
+    const int d0 = (b.kdop == 18) ? 4 : 0;  // 18-DOP uses the 6 edge directions only
+    for (int a = 0; a < nx; ++a) {
+      const int* d = dirs[d0 + a];
+      const size_t o = b.off_axes + 16ull * a;
+      const float org = rd<float>(b.p, o);
+      const int ex = rd<int32_t>(b.p, o + 4);
+      const int64_t root_lo = rd<int32_t>(b.p, o + 8), root_hi = rd<int32_t>(b.p, o + 12);
+      std::vector<int64_t> L(2ull * b.n_nodes, 0);
+      std::vector<double> plo(b.n_nodes, 1e300), phi(b.n_nodes, -1e300);
+      for (uint32_t n : order) {
+        const int64_t P0 = parent[n] < 0 ? root_lo : L[2ull * parent[n]];
+        const int64_t P1 = parent[n] < 0 ? root_hi : L[2ull * parent[n] + 1];
+        const uint32_t ql = code_field(b, n, 3 + a), qh = code_field(b, n, b.nax() + 3 + a);
+        if ((ql >> b.bits) || (qh >> b.bits)) report[0]++;
+        const int s = std::max(0, bitlen(P1 - P0) - (int)b.bits);
+        L[2ull * n] = P0 + ((int64_t)ql << s);
+        L[2ull * n + 1] = P1 - ((int64_t)qh << s);
+        if (L[2ull * n] < P0 || L[2ull * n + 1] > P1 || L[2ull * n] > L[2ull * n + 1]) report[2]++;
+      }
+      for (auto it = order.rbegin(); it != order.rend(); ++it) {
+        const uint32_t n = *it;
+        const uint32_t tp = blob_topo(b, n);
+        if (tp >> 31) {
+          const uint32_t first = tp & 0x1FFFFFFFu, cnt = ((tp >> 29) & 3u) + 1;
+          for (uint32_t k = 0; k < cnt && first + k < b.n_tris; ++k) {
+            const uint32_t ti = idx[first + k];
+            if ((int64_t)ti >= nt) continue;
+            for (int v = 0; v < 3; ++v) {
+              const float* x = &verts[3 * tris[3 * ti + v]];
+              const double pr = d[0] * (double)x[0] + d[1] * (double)x[1] + d[2] * (double)x[2];
+              plo[n] = std::min(plo[n], pr);
+              phi[n] = std::max(phi[n], pr);
+            }
+          }
+        }
+        if (parent[n] >= 0) {
+          plo[parent[n]] = std::min(plo[parent[n]], plo[n]);
+          phi[parent[n]] = std::max(phi[parent[n]], phi[n]);
+        }
+        const double lo = (double)org + std::ldexp((double)L[2ull * n], ex);
+        const double hi = (double)org + std::ldexp((double)L[2ull * n + 1], ex);
+        if (plo[n] < lo || phi[n] > hi) report[1]++;
+      }
+    }
+  }
   int64_t total = 0;
   for (int k = 0; k < 9; ++k) total += report[k];
   return total;

@@ -159,6 +159,9 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   if (T < branching || T > (1 << 20)) return set_error(CBVH_EINVAL, "treelet_nodes must be >= branching");
   if (c < 1 || c > 4) return set_error(CBVH_EINVAL, "leaf_size must be in [1, 4]");
   const int layout = opts ? opts->layout : CBVH_LAYOUT_DELTA;
+  const int kdop = (opts && opts->kdop) ? opts->kdop : 6;
+  if (kdop != 6 && kdop != 14 && kdop != 18 && kdop != 26) return set_error(CBVH_EINVAL, "kdop must be 6, 14, 18 or 26");
+  if (kdop != 6 && layout != CBVH_LAYOUT_DELTA) return set_error(CBVH_EINVAL, "k-DOPs use the delta layout");
   if (layout != CBVH_LAYOUT_DELTA && layout != CBVH_LAYOUT_FP16 && layout != CBVH_LAYOUT_FP32)
     return set_error(CBVH_EINVAL, "layout must be CBVH_LAYOUT_DELTA, _FP16 or _FP32");
   if (!mesh->vertices || !mesh->triangles) return set_error(CBVH_EINVAL, "null mesh arrays");
@@ -242,6 +245,94 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
           dec[6 * ch + 3 + a] = Phi - (qhi << s);
         }
         stack.push_back(ch);
+      }
+    }
+  }
+
+  // ---- k-DOP (Table I): k/2 - 3 extra slab directions,
+  // each on its own lattice (origin = fp32 floor of the root's min projection,
+  // cell 2^e_a), coded like the box axes against the decoded parent.
+  const int nx = kdop / 2 - 3;
+  std::vector<std::array<int, 3>> xdir;
+  if (kdop == 14 || kdop == 26) xdir.insert(xdir.end(), {{1, 1, 1}, {1, 1, -1}, {1, -1, 1}, {-1, 1, 1}});
+  if (kdop == 18 || kdop == 26)
+    xdir.insert(xdir.end(), {{1, 1, 0}, {1, -1, 0}, {1, 0, 1}, {1, 0, -1}, {0, 1, 1}, {0, 1, -1}});
+  std::vector<int64_t> xdec(2 * (size_t)nx * n), xcode_v(2 * (size_t)nx * n, 0);
+  std::vector<float> xorigin(nx);
+  std::vector<int> xexp(nx);
+  std::vector<int64_t> xroot(2 * (size_t)nx);
+  if (nx > 0) {
+    // exact projections (integer directions: sums of <= 3 fp32 values, exact
+    // in fp64), per node bottom-up (children have larger build ids)
+    std::vector<double> plo((size_t)nx * n, INFINITY), phi((size_t)nx * n, -INFINITY);
+    for (int i = n - 1; i >= 0; --i) {
+      const BNode& nd = bd.nodes[i];
+      if (nd.children.empty()) {
+        for (int k = nd.tri_begin; k < nd.tri_end; ++k)
+          for (int v = 0; v < 3; ++v) {
+            const float* x = &mesh->vertices[3 * (int64_t)mesh->triangles[3 * (int64_t)bd.perm[k] + v]];
+            for (int a = 0; a < nx; ++a) {
+              const double d = xdir[a][0] * (double)x[0] + xdir[a][1] * (double)x[1] + xdir[a][2] * (double)x[2];
+              plo[(size_t)a * n + i] = std::min(plo[(size_t)a * n + i], d);
+              phi[(size_t)a * n + i] = std::max(phi[(size_t)a * n + i], d);
+            }
+          }
+      } else {
+        for (int ch : nd.children)
+          for (int a = 0; a < nx; ++a) {
+            plo[(size_t)a * n + i] = std::min(plo[(size_t)a * n + i], plo[(size_t)a * n + ch]);
+            phi[(size_t)a * n + i] = std::max(phi[(size_t)a * n + i], phi[(size_t)a * n + ch]);
+          }
+      }
+    }
+    for (int a = 0; a < nx; ++a) {
+      const double rlo = plo[(size_t)a * n], rhi = phi[(size_t)a * n];
+      float o = (float)rlo;
+      if ((double)o > rlo) o = std::nextafter(o, -INFINITY);
+      const double ex = rhi - (double)o;
+      int ea = ex > 0 ? (int)std::ceil(std::log2(ex)) - 22 : -100;
+      ea = std::max(-100, std::min(100, ea));
+      while (std::ldexp(ex, -ea) > double(1 << 22)) ++ea;
+      xorigin[a] = o;
+      xexp[a] = ea;
+      auto at = [&](int64_t k) { return (double)o + std::ldexp((double)k, ea); };
+      auto llo = [&](double x) {
+        int64_t k = (int64_t)std::floor(std::ldexp(x - (double)o, -ea));
+        while (at(k) > x) --k;
+        while (at(k + 1) <= x) ++k;
+        return k;
+      };
+      auto lhi = [&](double x) {
+        int64_t k = (int64_t)std::ceil(std::ldexp(x - (double)o, -ea));
+        while (at(k) < x) ++k;
+        while (at(k - 1) >= x) --k;
+        return k;
+      };
+      std::vector<int64_t> L(2 * (size_t)n);
+      for (int i = 0; i < n; ++i) {
+        L[2 * i] = llo(plo[(size_t)a * n + i]);
+        L[2 * i + 1] = lhi(phi[(size_t)a * n + i]);
+      }
+      xroot[2 * a] = L[0];
+      xroot[2 * a + 1] = L[1];
+      xdec[((size_t)a * n + 0) * 2] = L[0];
+      xdec[((size_t)a * n + 0) * 2 + 1] = L[1];
+      std::vector<int> stack = {0};
+      while (!stack.empty()) {
+        int pn = stack.back(); stack.pop_back();
+        for (int ch : bd.nodes[pn].children) {
+          const int64_t Plo = xdec[((size_t)a * n + pn) * 2], Phi = xdec[((size_t)a * n + pn) * 2 + 1];
+          const int64_t Clo = L[2 * ch], Chi = L[2 * ch + 1];
+          if (Clo < Plo || Chi > Phi) return set_error(CBVH_EMESH, "internal: k-DOP child not inside decoded parent");
+          const int sh = std::max(0, bitlen64(Phi - Plo) - bits);
+          const int64_t qlo = (Clo - Plo) >> sh, qhi = (Phi - Chi) >> sh;
+          if (qlo >= (1 << bits) || qhi >= (1 << bits)) return set_error(CBVH_EMESH, "internal: correction overflow");
+          xcode_v[((size_t)a * n + ch) * 2] = qlo;
+          xcode_v[((size_t)a * n + ch) * 2 + 1] = qhi;
+          xdec[((size_t)a * n + ch) * 2] = Plo + (qlo << sh);
+          xdec[((size_t)a * n + ch) * 2 + 1] = Phi - (qhi << sh);
+          stack.push_back(ch);
+        }
       }
     }
   }
@@ -344,10 +435,12 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   // ---- serialize
   const uint32_t w = layout == CBVH_LAYOUT_FP32 ? 32u : layout == CBVH_LAYOUT_FP16 ? 16u
                    : bits <= 4 ? 4u : bits <= 8 ? 8u : 16u;
-  const size_t code_bytes_node = 6 * w / 8;
+  const int nax = kdop / 2;
+  const size_t code_bytes_node = 2 * (size_t)nax * w / 8;
   size_t off_topo = 256;
   size_t off_codes = align256(off_topo + 4 * (size_t)n);
-  size_t off_treelets = align256(off_codes + code_bytes_node * (size_t)n);
+  size_t off_axes = align256(off_codes + code_bytes_node * (size_t)n);
+  size_t off_treelets = align256(off_axes + 16 * (size_t)nx);
   size_t off_tris = align256(off_treelets + 32 * treelets.size());
   size_t off_tri_index = align256(off_tris + 48 * (size_t)nt);
   size_t total = align256(off_tri_index + 4 * (size_t)nt);
@@ -357,7 +450,7 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
     return set_error(CBVH_ENOMEM, "blob allocation failed");
   }
   std::memcpy(&out[0], "CBVH", 4);
-  put<uint32_t>(out, 4, 4u);
+  put<uint32_t>(out, 4, 5u);
   put<uint32_t>(out, 8, (uint32_t)branching);
   put<uint32_t>(out, 12, (uint32_t)bits);
   put<uint32_t>(out, 16, (uint32_t)T);
@@ -378,6 +471,15 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   put<uint64_t>(out, 120, off_tri_index);
   put<uint64_t>(out, 128, total);
   put<uint32_t>(out, 136, (uint32_t)layout);
+  put<uint32_t>(out, 140, (uint32_t)kdop);
+  put<uint64_t>(out, 144, off_axes);
+  for (int a = 0; a < nx; ++a) {
+    const size_t o = off_axes + 16 * (size_t)a;
+    put<float>(out, o, xorigin[a]);
+    put<int32_t>(out, o + 4, xexp[a]);
+    put<int32_t>(out, o + 8, (int32_t)xroot[2 * a]);
+    put<int32_t>(out, o + 12, (int32_t)xroot[2 * a + 1]);
+  }
   std::memcpy(&out[off_topo], topo.data(), 4 * (size_t)n);
   for (int nid = 0; nid < n; ++nid) {
     const uint16_t* q = &code[6 * (size_t)order[nid]];
@@ -398,14 +500,21 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
         put<uint16_t>(out, off_codes + code_bytes_node * nid + 2 * a, hl);
         put<uint16_t>(out, off_codes + code_bytes_node * nid + 6 + 2 * a, hh);
       }
-    } else if (w == 16) {
-      std::memcpy(dst, q, 12);
-    } else if (w == 8) {
-      for (int f = 0; f < 6; ++f) dst[f] = (uint8_t)q[f];
     } else {
-      uint32_t word = 0;
-      for (int f = 0; f < 6; ++f) word |= (uint32_t)(q[f] & 15u) << (4 * f);
-      dst[0] = word & 255u; dst[1] = (word >> 8) & 255u; dst[2] = (word >> 16) & 255u;
+      // fields lo[0..nax) then hi[0..nax): box axes x, y, z, then the k-DOP axes
+      std::vector<uint32_t> f(2 * (size_t)nax);
+      for (int a = 0; a < 3; ++a) { f[a] = q[a]; f[nax + a] = q[3 + a]; }
+      for (int a = 0; a < nx; ++a) {
+        f[3 + a] = (uint32_t)xcode_v[((size_t)a * n + order[nid]) * 2];
+        f[nax + 3 + a] = (uint32_t)xcode_v[((size_t)a * n + order[nid]) * 2 + 1];
+      }
+      if (w == 16) {
+        for (size_t k = 0; k < f.size(); ++k) { const uint16_t v = (uint16_t)f[k]; std::memcpy(dst + 2 * k, &v, 2); }
+      } else if (w == 8) {
+        for (size_t k = 0; k < f.size(); ++k) dst[k] = (uint8_t)f[k];
+      } else {
+        for (size_t k = 0; k < f.size(); k += 2) dst[k / 2] = (uint8_t)((f[k] & 15u) | ((f[k + 1] & 15u) << 4));
+      }
     }
   }
   for (size_t k = 0; k < treelets.size(); ++k) {
@@ -424,9 +533,13 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
   if (bytes < 256 || std::memcmp(p, "CBVH", 4) != 0) return set_error(CBVH_EBLOB, "bad magic");
   auto u32 = [&](size_t o) { uint32_t x; std::memcpy(&x, p + o, 4); return x; };
   auto u64 = [&](size_t o) { uint64_t x; std::memcpy(&x, p + o, 8); return x; };
-  if (u32(4) != 4) return set_error(CBVH_EBLOB, "unsupported blob version");
+  if (u32(4) != 5) return set_error(CBVH_EBLOB, "unsupported blob version");
   h->layout = u32(136);
   if (h->layout > 2) return set_error(CBVH_EBLOB, "bad layout");
+  h->kdop = u32(140);
+  h->off_axes = u64(144);
+  if (h->kdop != 6 && h->kdop != 14 && h->kdop != 18 && h->kdop != 26) return set_error(CBVH_EBLOB, "bad k");
+  if (h->kdop != 6 && h->layout != CBVH_LAYOUT_DELTA) return set_error(CBVH_EBLOB, "k-DOP with an absolute layout");
   h->branching = u32(8); h->bits = u32(12); h->treelet_nodes = u32(16); h->leaf_size = u32(20);
   h->code_width = u32(24); h->num_nodes = u32(28); h->num_tris = u32(32); h->num_treelets = u32(36);
   h->depth = u32(40); h->num_leaves = u32(44);
@@ -443,9 +556,9 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
   if (h->code_width != want_w) return set_error(CBVH_EBLOB, "bad code width");
   if (h->num_nodes == 0 || h->num_tris == 0 || h->num_nodes >= (1u << 28) || h->num_tris >= (1u << 29))
     return set_error(CBVH_EBLOB, "bad counts");
-  const uint64_t cb = 6ull * h->code_width / 8;
+  const uint64_t cb = (uint64_t)h->kdop * h->code_width / 8;
   if (h->off_topo < 256 || h->off_topo + 4ull * h->num_nodes > h->off_codes ||
-      h->off_codes + cb * h->num_nodes > h->off_treelets ||
+      h->off_codes + cb * h->num_nodes > h->off_axes || h->off_axes + 16ull * (h->kdop / 2 - 3) > h->off_treelets ||
       h->off_treelets + 32ull * h->num_treelets > h->off_tris ||
       h->off_tris + 48ull * h->num_tris > h->off_tri_index ||
       h->off_tri_index + 4ull * h->num_tris > h->total_bytes)
@@ -487,10 +600,11 @@ int cbvh_blob_info(const uint8_t* h_blob, size_t bytes, cbvh_info* out) {
   int rc = cbvh::parse_header(h_blob, bytes, &out->h);
   if (rc) return rc;
   const cbvh_header& h = out->h;
-  out->bvh_bytes = 4ull * h.num_nodes + (6ull * h.code_width / 8) * h.num_nodes + 32ull * h.num_treelets;
+  out->bvh_bytes = 4ull * h.num_nodes + ((uint64_t)h.kdop * h.code_width / 8) * h.num_nodes + 32ull * h.num_treelets +
+                   16ull * (h.kdop / 2 - 3);
   out->tri_bytes = 48ull * h.num_tris;
   out->bytes_per_node = (double)out->bvh_bytes / (double)h.num_nodes;
-  out->code_bytes_per_node = 6.0 * h.code_width / 8.0;
+  out->code_bytes_per_node = (double)h.kdop * h.code_width / 8.0;
   return CBVH_OK;
 }
 

@@ -1424,6 +1424,7 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
   cbvh_header h;
   int rc = parse_header(h_blob, bytes, &h);
   if (rc) return rc;
+  if (h.kdop != 6) return set_error(CBVH_EINVAL, "k-DOP blobs are not supported by the traversal kernel yet");
   // Topology validation (O(n)): children strictly after their parent (no
   // cycles, guaranteed by the builder's treelet numbering) and inside the node
   // array, leaf triangle ranges inside the soup — a corrupted blob must fail

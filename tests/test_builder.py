@@ -302,3 +302,74 @@ def test_leaf_slab_containment_and_fault(cfg1):
     dmin, dmax = np.frombuffer(bad[rec1 + 36:rec1 + 44].tobytes(), np.float32)
     bad[rec1 + 40:rec1 + 44] = np.frombuffer(np.float32(dmin + 0.25 * (dmax - dmin)).tobytes(), np.uint8)
     assert O.check_blob(bad, A.vertices, A.triangles)["containment"] > 0
+
+
+# ------------------------------------------------------------------ k-DOP nodes for the static model (§8(f))
+
+_KDOP_DIRS = {14: [(1, 1, 1), (1, 1, -1), (1, -1, 1), (-1, 1, 1)],
+              18: [(1, 1, 0), (1, -1, 0), (1, 0, 1), (1, 0, -1), (0, 1, 1), (0, 1, -1)]}
+_KDOP_DIRS[26] = _KDOP_DIRS[14] + _KDOP_DIRS[18]
+
+
+@pytest.mark.parametrize("kdop", [14, 18, 26])
+@pytest.mark.parametrize("B,bits", [(2, 4), (4, 8), (8, 16)])
+def test_kdop_invariants_and_aabb_part(cfg1, mesh16k, kdop, B, bits):
+    # every extra slab axis nests child-in-parent and contains the exact
+    # projections of its subtree (independent fp64 check); the x/y/z part of
+    # the codes is the AABB blob's, field for field
+    for m in (cfg1.B, mesh16k):
+        kb = M.build_compressed_bvh(m.vertices, m.triangles, B, bits, 32, 4, kdop=kdop)
+        r = O.check_blob(kb.blob, m.vertices, m.triangles)
+        assert r["violations"] == 0, r
+        ab = M.build_compressed_bvh(m.vertices, m.triangles, B, bits, 32, 4)
+        w, n, nax = kb.info["code_width"], kb.info["num_nodes"], kdop // 2
+        assert kb.info["kdop"] == kdop and kb.info["code_bytes_per_node"] == kdop * w // 8
+        def fields(bv, k):
+            c = bv.blob[bv.info["off_codes"]:bv.info["off_codes"] + n * k * w // 8]
+            if w == 16:
+                return np.frombuffer(c.tobytes(), np.uint16).reshape(n, k)
+            if w == 8:
+                return c.reshape(n, k)
+            c = c.reshape(n, k // 2)
+            return np.stack([c & 15, c >> 4], -1).reshape(n, k)
+        fk, fa = fields(kb, kdop), fields(ab, 6)
+        assert np.array_equal(fk[:, :3], fa[:, :3]) and np.array_equal(fk[:, nax:nax + 3], fa[:, 3:])
+
+
+@pytest.mark.parametrize("kdop", [14, 18, 26])
+def test_kdop_root_slabs_closed_form(kdop):
+    # axis table: the root interval of direction d is [min d.v, max d.v] of the
+    # mesh rounded outward by at most one cell 2^exp (exact fp64 projections)
+    rng = np.random.default_rng(7)
+    V = rng.normal(size=(30, 3)).astype(np.float32) * np.float32(3) + np.float32(10)
+    T = np.arange(30, dtype=np.int32).reshape(10, 3)
+    bv = M.build_compressed_bvh(V, T, 4, 8, 32, 4, kdop=kdop)
+    off = bv.info["off_axes"]
+    for a, d in enumerate(_KDOP_DIRS[kdop]):
+        rec = bv.blob[off + 16 * a:off + 16 * a + 16].tobytes()
+        org = float(np.frombuffer(rec[0:4], np.float32)[0])
+        ex, lo, hi = (int(x) for x in np.frombuffer(rec[4:16], np.int32))
+        pr = V.astype(np.float64) @ np.array(d, np.float64)
+        cell = 2.0 ** ex
+        assert org + lo * cell <= pr.min() < org + (lo + 1) * cell
+        assert org + (hi - 1) * cell < pr.max() <= org + hi * cell
+        assert hi - lo <= 2 ** 22
+    assert O.check_blob(bv.blob, V, T)["violations"] == 0
+
+
+def test_kdop_fault_and_errors(cfg1):
+    A = cfg1.B
+    bv = M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, 32, 4, kdop=14)
+    info = bv.info
+    topo = np.frombuffer(bv.blob[info["off_topo"]:info["off_topo"] + 4 * info["num_nodes"]].tobytes(), np.uint32)
+    leaf = int(np.nonzero(topo >> 31)[0][3])
+    bad = bv.blob.copy()
+    # a diagonal-axis correction of one leaf inflated: its slab no longer holds it
+    bad[info["off_codes"] + 14 * leaf + 3] = 255
+    bad[info["off_codes"] + 14 * leaf + 7 + 3] = 255
+    assert O.check_blob(bad, A.vertices, A.triangles)["containment"] > 0
+    for k in (8, 12, 20):
+        with pytest.raises(L.CbvhError, match="EINVAL"):
+            M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, kdop=k)
+    with pytest.raises(L.CbvhError, match="EINVAL"):
+        M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, layout="fp16", kdop=14)
