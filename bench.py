@@ -215,7 +215,8 @@ def run(args):
     if args.bits:
         w.bits = args.bits
     A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout)
-    B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout)
+    B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout,
+                               kdop=args.kdop)
     distance = w.mode == "distance"
     build_s = time.time() - t0
     A.to_device(dev)
@@ -282,7 +283,7 @@ def run(args):
                               "dumped": st["dumped"], "launches": M.last_launch_count(),
                               "timeline_ms": [t / 1e6 for t in st["timeline_ns"]],
                               "lane_util": st["bv_tests"] / max(1, 32 * st["iterations"]),
-                              "iterations": st["iterations"], "bv_tests": st["bv_tests"], "layout": args.layout, "early_exit": args.early_exit,
+                              "iterations": st["iterations"], "bv_tests": st["bv_tests"], "leaf_pairs": st["leaf_pairs"], "tri_tests": st["tri_tests"], "layout": args.layout, "kdop": args.kdop, "early_exit": args.early_exit,
                               "bytes_per_node": {"A": A.info["bytes_per_node"], "B": B.info["bytes_per_node"]}}), flush=True)
         return
 
@@ -334,7 +335,7 @@ def run(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": w.name, "poses_per_gpu": N, "A_tris": w.A.num_triangles,
                        "B_tris": w.B.num_triangles, "branching": w.branching, "bits": w.bits,
-                       "treelet_nodes": w.treelet, "leaf_size": w.leaf, "layout": args.layout,
+                       "treelet_nodes": w.treelet, "leaf_size": w.leaf, "layout": args.layout, "kdop_B": args.kdop,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"pose-sharded x{world} (independent batches)"},
             "bv_pair_tests_per_s": st["bv_tests"] / (statistics.median(step_ms) / 1e3),
@@ -380,6 +381,8 @@ def main():
                     help="pose preset; 'contact' = the paper's zero-distance preset (configs 1, 3)")
     ap.add_argument("--early-exit", action="store_true",
                     help="hit-only collide (stop each pose at its first hit); not the headline metric")
+    ap.add_argument("--kdop", type=int, default=6, choices=[6, 14, 18, 26],
+                    help="bounding volumes of the static model B: 6 = AABB, 14/18/26-DOP (delta layout)")
     ap.add_argument("--layout", default="delta", choices=["delta", "fp16", "fp32"],
                     help="node box layout (fp16/fp32: the paper's half-vs-float ablation)")
     ap.add_argument("--cpu-poses", type=int, default=100000)

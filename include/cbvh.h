@@ -125,6 +125,12 @@ typedef struct {
   uint32_t root_topo;      /* topology word of node 0 */
   int32_t root_decoded[6]; /* node 0 decoded against the header root box */
   float max_abs_coord;     /* max |coordinate| of the decoded root box (fp32 slack scale) */
+  /* k-DOP (kdop > 6): per extra slab axis a < kdop/2 - 3, the axis lattice
+   * (coordinate of index k along the direction: axis_origin[a] + k * 2^axis_exp[a])
+   * and node 0 decoded against the axis-table root interval */
+  float axis_origin[10];
+  int32_t axis_exp[10];
+  int32_t axis_root[20];   /* lo, hi per axis */
 } cbvh_bvh;
 
 /* Parse h_blob and bind it to d_blob.  Errors: CBVH_EINVAL, CBVH_EBLOB. */

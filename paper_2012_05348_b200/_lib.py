@@ -50,7 +50,8 @@ class cbvh_info(C.Structure):
 class cbvh_bvh(C.Structure):
     _fields_ = [("d_blob", C.c_void_p), ("bytes", C.c_size_t), ("h", cbvh_header),
                 ("root_topo", C.c_uint32), ("root_decoded", C.c_int32 * 6),
-                ("max_abs_coord", C.c_float)]
+                ("max_abs_coord", C.c_float), ("axis_origin", C.c_float * 10),
+                ("axis_exp", C.c_int32 * 10), ("axis_root", C.c_int32 * 20)]
 
 
 class cbvh_stats(C.Structure):

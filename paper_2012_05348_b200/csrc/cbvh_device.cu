@@ -66,6 +66,13 @@ struct DevTree {
   int32_t root[6];   // decoded root lattice box
 };
 
+// k-DOP slab axes of the static model B beyond x, y, z (kdop/2 - 3 <= 10):
+// per axis the lattice origin and cell
+struct KDopB {
+  float org[10], cell[10];
+  int32_t root[20];  // node 0 decoded (lo, hi per axis)
+};
+
 constexpr int kMaxPhases = 8;
 
 struct Control {
@@ -94,7 +101,9 @@ constexpr int kWarps = CBVH_WARPS;  // warps per CTA
 #define CBVH_STACK 96
 #endif
 constexpr int kStack = CBVH_STACK;  // smem stack entries per warp
-constexpr int kFields = 16;         // words per stack entry
+constexpr int kFields = 16;         // words per stack entry (AABB pairs)
+// words per stack entry with KX extra k-DOP axes on B (their decoded lo, hi)
+__host__ __device__ constexpr int nfields(int kx) { return kFields + 2 * kx; }
 constexpr int kLeafQ = 64;          // leaf-queue entries per warp
 constexpr int kSpillCap = 2048;     // global spill entries per warp
 constexpr int kContCap = 1 << 19;   // continuation-buffer items (per buffer, two buffers)
@@ -109,10 +118,11 @@ constexpr int kGrab = CBVH_GRAB;          // poses acquired per cursor atomic
 constexpr int kLowWater = CBVH_LOW_WATER; // acquire poses when the stack is below this
 
 // stack fields
-enum { F_POSE = 0, F_TA = 1, F_TB = 2, F_BA = 3, F_BB = 9, F_LB = 15 };
+enum { F_POSE = 0, F_TA = 1, F_TB = 2, F_BA = 3, F_BB = 9, F_LB = 15, F_XB = 16 };
 
 struct Params {
   DevTree A, B;
+  KDopB X;               // B's extra k-DOP axes (kernel instantiations with KX > 0)
   const float* poses;
   int N;
   uint8_t* hit;
@@ -249,6 +259,62 @@ struct PoseF {
   float t[3];
 };
 
+// ---------------------------------------------------------------- k-DOP (B)
+// Extra slab directions of a k-DOP (Table I; reading R22), in the
+// builder's order — 14: the 4 body diagonals; 18: the 6 edge directions;
+// 26: the diagonals, then the edges.  Integer components in {-1, 0, 1}.
+__host__ __device__ constexpr int diag_dir(int a, int k) {
+  // (1,1,1) (1,1,-1) (1,-1,1) (-1,1,1)
+  return a == 0 ? 1 : a == 1 ? (k == 2 ? -1 : 1) : a == 2 ? (k == 1 ? -1 : 1) : (k == 0 ? -1 : 1);
+}
+__host__ __device__ constexpr int edge_dir(int a, int k) {
+  // (1,1,0) (1,-1,0) (1,0,1) (1,0,-1) (0,1,1) (0,1,-1)
+  return k == (a < 4 ? 0 : 1) ? 1 : k == (a < 2 ? 1 : 2) ? ((a & 1) ? -1 : 1) : 0;
+}
+__host__ __device__ constexpr int kdop_dir(int kx, int a, int k) {
+  return (kx == 6 || (kx == 10 && a >= 4)) ? edge_dir(kx == 10 ? a - 4 : a, k) : diag_dir(a, k);
+}
+
+// the 2 * NAX stored fields of a k-DOP record: lo of the NAX axes, then hi
+template <int NAX>
+__device__ __forceinline__ void load_codes_k(const DevTree& T, uint32_t node, uint32_t q[2 * NAX]) {
+  if (T.width == 8) {
+    const unsigned short* p = reinterpret_cast<const unsigned short*>(T.codes + 2ull * NAX * node);
+    #pragma unroll
+    for (int i = 0; i < NAX; ++i) { const uint32_t a = __ldg(p + i); q[2 * i] = a & 255u; q[2 * i + 1] = a >> 8; }
+  } else if (T.width == 16) {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(T.codes + 4ull * NAX * node);
+    #pragma unroll
+    for (int i = 0; i < NAX; ++i) { const uint32_t a = __ldg(p + i); q[2 * i] = a & 0xffffu; q[2 * i + 1] = a >> 16; }
+  } else {
+    const uint8_t* p = T.codes + (uint64_t)NAX * node;
+    #pragma unroll
+    for (int i = 0; i < NAX; ++i) { const uint32_t a = __ldg(p + i); q[2 * i] = a & 15u; q[2 * i + 1] = a >> 4; }
+  }
+}
+
+// child k-DOP from the decoded parent (box P, extra axes PX): the same
+// predictor-corrector step per axis as decode_child
+template <int KX>
+__device__ __forceinline__ void fetch_child_kdop(const DevTree& T, uint32_t node, const int32_t P[6],
+                                                 const int32_t* PX, int32_t C[6], int32_t* CX) {
+  constexpr int NAX = 3 + KX;
+  uint32_t q[2 * NAX];
+  load_codes_k<NAX>(T, node, q);
+  #pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int s = max(0, (32 - __clz(P[3 + a] - P[a])) - T.bits);
+    C[a] = P[a] + (int32_t)(q[a] << s);
+    C[3 + a] = P[3 + a] - (int32_t)(q[NAX + a] << s);
+  }
+  #pragma unroll
+  for (int a = 0; a < KX; ++a) {
+    const int s = max(0, (32 - __clz(PX[2 * a + 1] - PX[2 * a])) - T.bits);
+    CX[2 * a] = PX[2 * a] + (int32_t)(q[3 + a] << s);
+    CX[2 * a + 1] = PX[2 * a + 1] - (int32_t)(q[NAX + 3 + a] << s);
+  }
+}
+
 __device__ __forceinline__ PoseF load_pose(const float* poses, int i) {
   const float4* p = reinterpret_cast<const float4*>(poses + 12ll * i);
   float4 r0 = __ldg(p), r1 = __ldg(p + 1), r2 = __ldg(p + 2);
@@ -297,6 +363,39 @@ __device__ __forceinline__ float sat_gap(const PoseF& P, const float alo[3], con
     *lb = fmaxf(fmaxf(e, gmax), 0.f) - eps;
   }
   return gmax - eps;
+}
+
+// A's box (A-local, under pose P) against B's extra k-DOP slabs: the gap
+// along each direction d (unnormalised, |d|_1 <= 3) between the projection
+// interval of the posed box and B's slab, less |d|_1 eps for the rounding of
+// the projections, divided by |d|_2 (reciprocal rounded down) — a lower bound
+// on the separation along the unit direction; > 0 means separated.
+template <int KX>
+__device__ __forceinline__ float kdop_gap(const PoseF& P, const float alo[3], const float ahi[3],
+                                          const KDopB& X, const int32_t* CX, float eps) {
+  float ca[3], ha[3], wc[3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    ca[k] = 0.5f * (alo[k] + ahi[k]);
+    ha[k] = 0.5f * (ahi[k] - alo[k]);
+  }
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) wc[k] = fmaf(P.R[k][0], ca[0], fmaf(P.R[k][1], ca[1], fmaf(P.R[k][2], ca[2], P.t[k])));
+  float g = -FLT_MAX;
+  #pragma unroll
+  for (int a = 0; a < KX; ++a) {
+    const float d0 = (float)kdop_dir(KX, a, 0), d1 = (float)kdop_dir(KX, a, 1), d2 = (float)kdop_dir(KX, a, 2);
+    const float c = d0 * wc[0] + d1 * wc[1] + d2 * wc[2];
+    float r = 0.f;
+    #pragma unroll
+    for (int i = 0; i < 3; ++i) r = fmaf(fabsf(d0 * P.R[0][i] + d1 * P.R[1][i] + d2 * P.R[2][i]), ha[i], r);
+    const float xlo = __fmaf_rd(__int2float_rn(CX[2 * a]), X.cell[a], X.org[a]);
+    const float xhi = __fmaf_ru(__int2float_rn(CX[2 * a + 1]), X.cell[a], X.org[a]);
+    const float gap = fmaxf(xlo - (c + r), (c - r) - xhi);
+    const bool diag = kdop_dir(KX, a, 0) != 0 && kdop_dir(KX, a, 1) != 0 && kdop_dir(KX, a, 2) != 0;
+    g = fmaxf(g, (gap - (diag ? 3.f : 2.f) * eps) * (diag ? 0.57735020f : 0.70710670f));
+  }
+  return g;
 }
 
 // ---------------------------------------------------------------- leaf tests
@@ -569,7 +668,9 @@ __device__ __noinline__ float tri_dist_fp64(const PoseF& P, const float* trisA, 
 
 constexpr int kSurv = 64;  // exact-test queue entries per warp (pose, tri A, tri B)
 // per-warp shared memory: stack + leaf queue (+ the exact-test queue, distance only)
-__host__ __device__ constexpr int warp_smem_words(int mode) { return kFields * kStack + 5 * kLeafQ + (mode == 1 ? 3 * kSurv : 0); }
+__host__ __device__ constexpr int warp_smem_words(int mode, int kx) {
+  return nfields(kx) * kStack + 5 * kLeafQ + (mode == 1 ? 3 * kSurv : 0);
+}
 
 // child pairs of an item: Alg. 1 enumerates children of every side it
 // descends (flags chosen at push time, see descent_flags)
@@ -603,10 +704,10 @@ __device__ __forceinline__ uint32_t full_mask(uint32_t t) { return (2u << ((t >>
 
 // per-warp constant context (registers); mutable counters live in the kernel
 struct WarpCtx {
-  uint32_t* st;     // stack SoA [kFields][kStack]
+  uint32_t* st;     // stack SoA [nfields(KX)][kStack]
   uint32_t* lq;     // leaf queue SoA [5][kLeafQ]: pose, topoA, topoB, triangle lists, lower bound (distance)
   uint32_t* sq;     // exact-test queue SoA [3][kSurv]: pose, triangle of A, triangle of B
-  uint32_t* spill;  // this warp's global spill area [kSpillCap][kFields]
+  uint32_t* spill;  // this warp's global spill area [kSpillCap][nfields(KX)]
   int lane;
 };
 
@@ -802,6 +903,7 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
 
 // Move the bottom half of the smem stack to the warp's global spill area.
 // Returns the new (top, spill_top); on overflow flags CBVH_EOVERFLOW.
+template <int NF>
 __device__ __noinline__ int2 spill_out(const Params& p, const WarpCtx c, int top, int spill_top) {
   constexpr int H = kStack / 2;
   if (spill_top + H > kSpillCap) {
@@ -809,13 +911,13 @@ __device__ __noinline__ int2 spill_out(const Params& p, const WarpCtx c, int top
     return make_int2(0, spill_top);  // abandon; cbvh_check reports the error
   }
   __syncwarp();
-  for (int idx = c.lane; idx < H * kFields; idx += 32) {
-    int e = idx / kFields, f = idx % kFields;
-    c.spill[(size_t)(spill_top + e) * kFields + f] = c.st[f * kStack + e];
+  for (int idx = c.lane; idx < H * NF; idx += 32) {
+    int e = idx / NF, f = idx % NF;
+    c.spill[(size_t)(spill_top + e) * NF + f] = c.st[f * kStack + e];
   }
   __syncwarp();
   const int rest = top - H;
-  for (int idx = c.lane; idx < rest * kFields; idx += 32) {
+  for (int idx = c.lane; idx < rest * NF; idx += 32) {
     int e = idx % rest, f = idx / rest;
     c.st[f * kStack + e] = c.st[f * kStack + e + H];
   }
@@ -824,13 +926,14 @@ __device__ __noinline__ int2 spill_out(const Params& p, const WarpCtx c, int top
 }
 
 // Refill an empty smem stack from the top of the spill area.
+template <int NF>
 __device__ __noinline__ int2 spill_in(const WarpCtx c, int spill_top) {
   const int n = min(kStack / 2, spill_top);
   const int base = spill_top - n;
   __syncwarp();
-  for (int idx = c.lane; idx < n * kFields; idx += 32) {
-    int e = idx / kFields, f = idx % kFields;
-    c.st[f * kStack + e] = c.spill[(size_t)(base + e) * kFields + f];
+  for (int idx = c.lane; idx < n * NF; idx += 32) {
+    int e = idx / NF, f = idx % NF;
+    c.st[f * kStack + e] = c.spill[(size_t)(base + e) * NF + f];
   }
   __syncwarp();
   return make_int2(n, base);
@@ -861,30 +964,38 @@ __device__ __forceinline__ int reserve_cont(unsigned* count, int n, int lane) {
 }
 
 // Dump the smem stack and the spill area; false if the buffer is full.
+template <int NF>
 __device__ __noinline__ bool dump_items(const Params& p, const WarpCtx c, int top, int spill_top) {
   const int n = top + spill_top;
   const int base = reserve_cont(&p.ctl->count[p.phase], n, c.lane);
   if (base < 0) return false;
-  uint32_t* out = p.cont_out + (size_t)base * kFields;
-  for (int idx = c.lane; idx < spill_top * kFields; idx += 32) out[idx] = c.spill[idx];
-  out += (size_t)spill_top * kFields;
-  for (int idx = c.lane; idx < top * kFields; idx += 32) {
-    const int e = idx / kFields, f = idx % kFields;
+  uint32_t* out = p.cont_out + (size_t)base * NF;
+  for (int idx = c.lane; idx < spill_top * NF; idx += 32) out[idx] = c.spill[idx];
+  out += (size_t)spill_top * NF;
+  for (int idx = c.lane; idx < top * NF; idx += 32) {
+    const int e = idx / NF, f = idx % NF;
     out[idx] = c.st[f * kStack + e];
   }
   return true;
 }
 
-template <int MODE, bool STATS>
-__global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBVH_MIN_BLOCKS_DIST) traverse_kernel(const __grid_constant__ Params p) {
+// resident CTAs per SM the register allocation targets (k-DOP stacks take
+// more shared memory and registers)
+__host__ __device__ constexpr int min_blocks(int mode, int kx) {
+  return kx == 0 ? (mode == 0 ? CBVH_MIN_BLOCKS : CBVH_MIN_BLOCKS_DIST) : (mode == 0 ? (kx >= 10 ? 3 : 4) : 3);
+}
+
+template <int MODE, bool STATS, int KX>
+__global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_kernel(const __grid_constant__ Params p) {
+  constexpr int NF = nfields(KX);
   extern __shared__ uint32_t smem[];
   const int wib = threadIdx.x >> 5;
   WarpCtx c;
   c.lane = threadIdx.x & 31;
-  c.st = smem + wib * warp_smem_words(MODE);
-  c.lq = c.st + kFields * kStack;
+  c.st = smem + wib * warp_smem_words(MODE, KX);
+  c.lq = c.st + NF * kStack;
   c.sq = c.lq + 5 * kLeafQ;
-  c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * kFields;
+  c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * NF;
   int top = 0, nleaf = 0, spill_top = 0;
   int after = 0;  // iterations since the input ran out
   unsigned long long s_dump = 0, s_iter = 0;
@@ -940,6 +1051,8 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
                 c.st[(F_BA + q) * kStack + slot] = (uint32_t)p.A.root[q];
                 c.st[(F_BB + q) * kStack + slot] = (uint32_t)p.B.root[q];
               }
+              #pragma unroll
+              for (int q = 0; q < 2 * KX; ++q) c.st[(F_XB + q) * kStack + slot] = (uint32_t)p.X.root[q];
               c.st[F_LB * kStack + slot] = 0u;
             }
           }
@@ -960,9 +1073,9 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
           poses_left = false;
         } else {
           const int k = min(kGrabItems, (int)(avail - base));
-          for (int idx = c.lane; idx < k * kFields; idx += 32) {
-            const int e = idx / kFields, f = idx % kFields;
-            c.st[f * kStack + top + e] = p.cont_in[(size_t)(base + e) * kFields + f];
+          for (int idx = c.lane; idx < k * NF; idx += 32) {
+            const int e = idx / NF, f = idx % NF;
+            c.st[f * kStack + top + e] = p.cont_in[(size_t)(base + e) * NF + f];
           }
           top += k;
           __syncwarp();
@@ -971,7 +1084,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
     }
     if (top == 0) {
       if (spill_top > 0) {
-        int2 r = spill_in(c, spill_top);
+        int2 r = spill_in<NF>(c, spill_top);
         top = r.x; spill_top = r.y;
         continue;
       }
@@ -984,7 +1097,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
         s_tri += drain_leaves<MODE>(p, c, nleaf);
         nleaf = 0;
       }
-      if (dump_items(p, c, top, spill_top)) {
+      if (dump_items<NF>(p, c, top, spill_top)) {
         if (STATS) s_dump += top + spill_top;
         top = 0;
         spill_top = 0;
@@ -1025,12 +1138,14 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
     const uint32_t pose = pword & kPoseMask;
     const uint32_t ta = c.st[F_TA * kStack + slot];
     const uint32_t tb = c.st[F_TB * kStack + slot];
-    int32_t BA[6], BB[6];
+    int32_t BA[6], BB[6], BX[2 * KX + 1];
     #pragma unroll
     for (int q = 0; q < 6; ++q) {
       BA[q] = (int32_t)c.st[(F_BA + q) * kStack + slot];
       BB[q] = (int32_t)c.st[(F_BB + q) * kStack + slot];
     }
+    #pragma unroll
+    for (int q = 0; q < 2 * KX; ++q) BX[q] = (int32_t)c.st[(F_XB + q) * kStack + slot];
     const float item_lb = __uint_as_float(c.st[F_LB * kStack + slot]);
     __syncwarp();
     top -= m;
@@ -1052,7 +1167,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
       if (MODE == 1) valid = valid && item_lb < best;
       if (MODE == 0 && p.early_exit) valid = valid && !early_done;
       const int i = small_div(k, nb), j = k - i * nb;
-      int32_t CA[6], CB[6];
+      int32_t CA[6], CB[6], CX[2 * KX + 1];
       uint32_t cta = ta, ctb = tb;
       bool surv = false;
       float lb = 0.f;
@@ -1072,16 +1187,22 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
           uint32_t node = (tb & 0x0FFFFFFFu) + (uint32_t)j;
           CBVH_GUARD(p, node < p.B.n_nodes, (node = 0, bad = true));
           ctb = __ldg(p.B.topo + node);
-          fetch_child_box(p.B, node, BB, CB);
+          if constexpr (KX > 0) fetch_child_kdop<KX>(p.B, node, BB, BX, CB, CX);
+          else fetch_child_box(p.B, node, BB, CB);
         } else {
           #pragma unroll
           for (int r = 0; r < 6; ++r) CB[r] = BB[r];
+          #pragma unroll
+          for (int r = 0; r < 2 * KX; ++r) CX[r] = BX[r];
         }
         float alo[3], ahi[3], blo[3], bhi[3];
         words_to_float(p.A, CA, alo, ahi);
         words_to_float(p.B, CB, blo, bhi);
         if (MODE == 0) {
           surv = sat_gap<false>(P, alo, ahi, blo, bhi, eps, nullptr) <= 0.f;
+          if constexpr (KX > 0) {
+            if (surv) surv = kdop_gap<KX>(P, alo, ahi, p.X, CX, eps) <= 0.f;
+          }
           // Against a leaf, "intersect" is refined to the leaf's triangles
           // themselves (still conservative): the partner's box must touch at
           // least one of them.  B's leaves are ~10x A's in config 5, so the
@@ -1112,11 +1233,14 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
           }
         } else {
           sat_gap<true>(P, alo, ahi, blo, bhi, eps, &lb);
+          if constexpr (KX > 0) {
+            if (lb < best) lb = fmaxf(lb, kdop_gap<KX>(P, alo, ahi, p.X, CX, eps));
+          }
           surv = lb < best;
         }
         if (STATS) {
           s_dec += (a_int ? 1 : 0) + (b_int ? 1 : 0);
-          s_rec += (a_int ? 4 + 3 * p.A.width / 4 : 0) + (b_int ? 4 + 3 * p.B.width / 4 : 0);
+          s_rec += (a_int ? 4 + 3 * p.A.width / 4 : 0) + (b_int ? 4 + (3 + KX) * p.B.width / 4 : 0);
         }
       }
       if (bad) surv = false;
@@ -1127,7 +1251,7 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
       const unsigned pm = __ballot_sync(FULL, push);
       if (pm) {
         if (top + 32 > kStack) {
-          int2 r = spill_out(p, c, top, spill_top);
+          int2 r = spill_out<NF>(p, c, top, spill_top);
           top = r.x; spill_top = r.y;
           if (STATS) s_spill++;
         }
@@ -1152,6 +1276,8 @@ __global__ void __launch_bounds__(kWarps * 32, MODE == 0 ? CBVH_MIN_BLOCKS : CBV
             c.st[(F_BA + q) * kStack + s2] = (uint32_t)CA[q];
             c.st[(F_BB + q) * kStack + s2] = (uint32_t)CB[q];
           }
+          #pragma unroll
+          for (int q = 0; q < 2 * KX; ++q) c.st[(F_XB + q) * kStack + s2] = (uint32_t)CX[q];
           if (MODE == 1) c.st[F_LB * kStack + s2] = __float_as_uint(lb);
         }
         top += __popc(pm);
@@ -1256,14 +1382,14 @@ static int cuda_fail(cudaError_t e, const char* what) {
   return CBVH_ECUDA;
 }
 
-static size_t smem_bytes(int mode) { return (size_t)kWarps * warp_smem_words(mode) * sizeof(uint32_t); }
+static size_t smem_bytes(int mode, int kx) { return (size_t)kWarps * warp_smem_words(mode, kx) * sizeof(uint32_t); }
 
 struct LaunchShape {
   int blocks;
   int warps;
 };
 
-template <int MODE, bool STATS>
+template <int MODE, bool STATS, int KX>
 static int shape_for(LaunchShape* s) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -1272,9 +1398,13 @@ static int shape_for(LaunchShape* s) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(traverse_kernel<MODE, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(MODE));
+    e = cudaFuncSetAttribute(traverse_kernel<MODE, STATS, KX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_bytes(MODE, KX));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    attr_set = true;
   }
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel<MODE, STATS>, kWarps * 32, smem_bytes(MODE));
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel<MODE, STATS, KX>, kWarps * 32,
+                                                    smem_bytes(MODE, KX));
   if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
   if (per_sm < 1) per_sm = 1;
   s->blocks = sms * per_sm;
@@ -1282,20 +1412,34 @@ static int shape_for(LaunchShape* s) {
   return CBVH_OK;
 }
 
-static int max_warps(int mode) {
+template <int KX>
+static int max_warps_kx(int mode) {
   // workspace is sized for the larger of the instantiations of this mode
   LaunchShape a{}, b{};
-  int rc = mode == 0 ? shape_for<0, false>(&a) : shape_for<1, false>(&a);
+  int rc = mode == 0 ? shape_for<0, false, KX>(&a) : shape_for<1, false, KX>(&a);
   if (rc) return -1;
-  rc = mode == 0 ? shape_for<0, true>(&b) : shape_for<1, true>(&b);
+  rc = mode == 0 ? shape_for<0, true, KX>(&b) : shape_for<1, true, KX>(&b);
   if (rc) return -1;
   return a.warps > b.warps ? a.warps : b.warps;
 }
 
-static size_t workspace_for_warps(int warps) {
-  return 256 + (size_t)warps * kSpillCap * kFields * sizeof(uint32_t) +
-         2 * (size_t)kContCap * kFields * sizeof(uint32_t);
+static int max_warps(int mode, int kx) {
+  switch (kx) {
+    case 0: return max_warps_kx<0>(mode);
+    case 4: return max_warps_kx<4>(mode);
+    case 6: return max_warps_kx<6>(mode);
+    case 10: return max_warps_kx<10>(mode);
+  }
+  return -1;
 }
+
+static size_t workspace_for_warps(int warps, int kx) {
+  return 256 + (size_t)warps * kSpillCap * nfields(kx) * sizeof(uint32_t) +
+         2 * (size_t)kContCap * nfields(kx) * sizeof(uint32_t);
+}
+
+// extra k-DOP axes of B (0 for an AABB blob)
+static int extra_axes(const cbvh_bvh* B) { return B ? (int)B->h.kdop / 2 - 3 : 0; }
 
 // Phase schedule: budgets of the bounded phases, then one
 // unbounded phase.  CBVH_PHASES="b0,b1,..." overrides (tuning only).
@@ -1339,10 +1483,10 @@ static DevTree make_tree(const cbvh_bvh* T) {
   return d;
 }
 
-template <int MODE, bool STATS>
-static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
-                  uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream, int descent,
-                  int early_exit) {
+template <int MODE, bool STATS, int KX>
+static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
+                     uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream, int descent,
+                     int early_exit) {
   g_launches = 0;
   if (!A || !B || !d_ws) return set_error(CBVH_EINVAL, "null argument");
   if (N < 0 || N > 0x3fffffffLL) return set_error(CBVH_EINVAL, "N out of range [0, 2^30)");
@@ -1355,9 +1499,9 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
   if ((reinterpret_cast<uintptr_t>(d_poses) & 15) != 0) return set_error(CBVH_EINVAL, "poses must be 16-byte aligned");
   if ((reinterpret_cast<uintptr_t>(d_ws) & 255) != 0) return set_error(CBVH_EINVAL, "workspace must be 256-byte aligned");
   LaunchShape s;
-  int rc = shape_for<MODE, STATS>(&s);
+  int rc = shape_for<MODE, STATS, KX>(&s);
   if (rc) return rc;
-  if (ws_bytes < workspace_for_warps(s.warps)) return set_error(CBVH_EWORKSPACE, "workspace too small");
+  if (ws_bytes < workspace_for_warps(s.warps, KX)) return set_error(CBVH_EWORKSPACE, "workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Params p;
   p.A = make_tree(A);
@@ -1368,6 +1512,13 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
   p.B.root_topo = B->root_topo;
   p.A.maxabs = A->max_abs_coord;
   p.B.maxabs = B->max_abs_coord;
+  std::memset(&p.X, 0, sizeof p.X);
+  for (int a = 0; a < KX; ++a) {
+    p.X.org[a] = B->axis_origin[a];
+    p.X.cell[a] = std::ldexp(1.0f, B->axis_exp[a]);
+    p.X.root[2 * a] = B->axis_root[2 * a];
+    p.X.root[2 * a + 1] = B->axis_root[2 * a + 1];
+  }
   p.poses = d_poses;
   p.N = (int)N;
   p.hit = d_hit;
@@ -1375,8 +1526,8 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
   p.dist_bits = reinterpret_cast<uint32_t*>(d_dist);
   p.ctl = static_cast<Control*>(d_ws);
   p.spill = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + 256);
-  uint32_t* cont0 = p.spill + (size_t)s.warps * kSpillCap * kFields;
-  uint32_t* cont1 = cont0 + (size_t)kContCap * kFields;
+  uint32_t* cont0 = p.spill + (size_t)s.warps * kSpillCap * nfields(KX);
+  uint32_t* cont1 = cont0 + (size_t)kContCap * nfields(KX);
   p.descent = descent;
   p.early_exit = (MODE == 0 && early_exit) ? 1 : 0;
   p.nwarps = s.warps;
@@ -1395,13 +1546,31 @@ static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
     p.budget = ph < nb ? budgets[ph] : -1;
     p.cont_in = (ph & 1) ? cont0 : cont1;   // phase ph reads what ph - 1 wrote
     p.cont_out = (ph & 1) ? cont1 : cont0;
-    traverse_kernel<MODE, STATS><<<s.blocks, kWarps * 32, smem_bytes(MODE), st>>>(p);
+    traverse_kernel<MODE, STATS, KX><<<s.blocks, kWarps * 32, smem_bytes(MODE, KX), st>>>(p);
     g_launches++;
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "traverse_kernel launch");
   }
   if (g_ev_stop) cudaEventRecord(g_ev_stop, st);
   return CBVH_OK;
+}
+
+// k-DOPs bound the static model B only (reading R22): the kernel is
+// instantiated per number of B's extra slab axes
+template <int MODE, bool STATS>
+static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
+                  uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream, int descent,
+                  int early_exit) {
+  g_launches = 0;
+  if (!A || !B) return set_error(CBVH_EINVAL, "null argument");
+  if (A->h.kdop != 6) return set_error(CBVH_EINVAL, "k-DOP blobs bound the static model B only; A must be an AABB blob");
+  switch (extra_axes(B)) {
+    case 0: return launch_kx<MODE, STATS, 0>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit);
+    case 4: return launch_kx<MODE, STATS, 4>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit);
+    case 6: return launch_kx<MODE, STATS, 6>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit);
+    case 10: return launch_kx<MODE, STATS, 10>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit);
+  }
+  return set_error(CBVH_EINVAL, "bad k-DOP");
 }
 
 }  // namespace cbvh
@@ -1424,7 +1593,6 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
   cbvh_header h;
   int rc = parse_header(h_blob, bytes, &h);
   if (rc) return rc;
-  if (h.kdop != 6) return set_error(CBVH_EINVAL, "k-DOP blobs are not supported by the traversal kernel yet");
   // Topology validation (O(n)): children strictly after their parent (no
   // cycles, guaranteed by the builder's treelet numbering) and inside the node
   // array, leaf triangle ranges inside the soup — a corrupted blob must fail
@@ -1446,6 +1614,7 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
       }
     }
   }
+  std::memset(out, 0, sizeof *out);
   out->d_blob = d_blob;
   out->bytes = bytes;
   out->h = h;
@@ -1471,24 +1640,39 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
     return CBVH_OK;
   }
   // node 0 is coded against the header root box (the anchor of treelet 0)
-  uint32_t q[6];
+  // and, for a k-DOP, against the axis table's root intervals.  Stored fields:
+  // lo of the k/2 axes, then hi (4-bit fields two per byte, low nibble first).
+  const int nax = (int)h.kdop / 2;
   const uint8_t* c = h_blob + h.off_codes;
-  if (h.code_width == 16) {
-    for (int f = 0; f < 6; ++f) { uint16_t x; std::memcpy(&x, c + 2 * f, 2); q[f] = x; }
-  } else if (h.code_width == 8) {
-    for (int f = 0; f < 6; ++f) q[f] = c[f];
-  } else {
-    uint32_t w = c[0] | (c[1] << 8) | (c[2] << 16);
-    for (int f = 0; f < 6; ++f) q[f] = (w >> (4 * f)) & 15u;
-  }
-  for (int a = 0; a < 3; ++a) {
-    int64_t E = (int64_t)h.root_box[3 + a] - h.root_box[a];
-    if (E < 0 || E >= (1ll << 23)) return set_error(CBVH_EBLOB, "bad root box");
+  auto field = [&](int f) -> uint32_t {
+    if (h.code_width == 16) { uint16_t x; std::memcpy(&x, c + 2 * f, 2); return x; }
+    if (h.code_width == 8) return c[f];
+    return (c[f / 2] >> (4 * (f % 2))) & 15u;
+  };
+  auto decode = [&](int64_t lo, int64_t hi, uint32_t qlo, uint32_t qhi, int32_t* dlo, int32_t* dhi) {
+    const int64_t E = hi - lo;
+    if (E < 0 || E >= (1ll << 23)) return false;
     int bl = 0;
     while ((E >> bl) > 0) ++bl;
-    int s = bl - (int)h.bits > 0 ? bl - (int)h.bits : 0;
-    out->root_decoded[a] = h.root_box[a] + (int32_t)(q[a] << s);
-    out->root_decoded[3 + a] = h.root_box[3 + a] - (int32_t)(q[3 + a] << s);
+    const int s = bl - (int)h.bits > 0 ? bl - (int)h.bits : 0;
+    *dlo = (int32_t)(lo + ((int64_t)qlo << s));
+    *dhi = (int32_t)(hi - ((int64_t)qhi << s));
+    return true;
+  };
+  for (int a = 0; a < 3; ++a)
+    if (!decode(h.root_box[a], h.root_box[3 + a], field(a), field(nax + a), &out->root_decoded[a],
+                &out->root_decoded[3 + a]))
+      return set_error(CBVH_EBLOB, "bad root box");
+  for (int a = 0; a < nax - 3; ++a) {
+    const uint8_t* t = h_blob + h.off_axes + 16ull * a;
+    int32_t rlo, rhi;
+    std::memcpy(&out->axis_origin[a], t, 4);
+    std::memcpy(&out->axis_exp[a], t + 4, 4);
+    std::memcpy(&rlo, t + 8, 4);
+    std::memcpy(&rhi, t + 12, 4);
+    if (out->axis_exp[a] < -126 || out->axis_exp[a] > 127 || !std::isfinite(out->axis_origin[a]) || rlo < 0 || rhi >= (1 << 24) ||
+        !decode(rlo, rhi, field(3 + a), field(nax + 3 + a), &out->axis_root[2 * a], &out->axis_root[2 * a + 1]))
+      return set_error(CBVH_EBLOB, "bad k-DOP axis table");
   }
   float m = 0.f;
   for (int a = 0; a < 3; ++a) {
@@ -1502,9 +1686,10 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
 
 size_t cbvh_workspace_bytes(const cbvh_bvh* A, const cbvh_bvh* B, int64_t N, int mode) {
   (void)A; (void)B; (void)N;
-  int w = max_warps(mode == 1 ? 1 : 0);
+  const int kx = extra_axes(B);
+  int w = max_warps(mode == 1 ? 1 : 0, kx);
   if (w <= 0) return 0;
-  return workspace_for_warps(w);
+  return workspace_for_warps(w, kx);
 }
 
 static int opts_descent(const cbvh_query_opts* o) { return o ? o->descent : CBVH_DESCENT_LARGER; }

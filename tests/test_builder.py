@@ -373,3 +373,25 @@ def test_kdop_fault_and_errors(cfg1):
             M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, kdop=k)
     with pytest.raises(L.CbvhError, match="EINVAL"):
         M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, layout="fp16", kdop=14)
+
+
+def test_bind_kdop_axis_table(cfg1):
+    # cbvh_bind reads the axis table and decodes node 0 of every extra axis
+    # (no device access: bind only records the device pointer)
+    B = cfg1.B
+    lib = L.load()
+    fake_dev = C.c_void_p(1 << 20)
+    for k in (14, 18, 26):
+        bv = M.build_compressed_bvh(B.vertices, B.triangles, 4, 8, 32, 4, kdop=k)
+        out = L.cbvh_bvh()
+        rc = lib.cbvh_bind(bv.blob.ctypes.data_as(C.POINTER(C.c_uint8)), bv.blob.nbytes, fake_dev, C.byref(out))
+        assert rc == L.CBVH_OK
+        off = bv.info["off_axes"]
+        for a in range(k // 2 - 3):
+            rec = np.frombuffer(bv.blob[off + 16 * a:off + 16 * a + 16].tobytes(), np.int32)
+            assert out.axis_exp[a] == rec[1]
+            assert out.axis_root[2 * a] == rec[2] and out.axis_root[2 * a + 1] == rec[3]  # node 0 == table root
+        bad = bv.blob.copy()
+        bad[off + 4:off + 8] = np.frombuffer(np.int32(500).tobytes(), np.uint8)  # absurd exponent
+        rc = lib.cbvh_bind(bad.ctypes.data_as(C.POINTER(C.c_uint8)), bad.nbytes, fake_dev, C.byref(out))
+        assert rc == L.CBVH_EBLOB

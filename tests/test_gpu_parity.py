@@ -53,8 +53,9 @@ def run_distance(M, A, B, poses, stats=False, descent="larger"):
     return out
 
 
-def build(M, mesh, B, bits, T=32, layout="delta"):
-    return M.build_compressed_bvh(mesh.vertices, mesh.triangles, B, bits, T, 4, layout=layout).to_device()
+def build(M, mesh, B, bits, T=32, layout="delta", kdop=6):
+    return M.build_compressed_bvh(mesh.vertices, mesh.triangles, B, bits, T, 4, layout=layout,
+                                  kdop=kdop).to_device()
 
 
 def oracle_trees(w):
@@ -121,6 +122,35 @@ def test_config1_absolute_layouts(M, cfg1, layout):
     d = run_distance(M, A, B, w.poses[:128])
     d64, _ = O.distance(tA, tB, w.poses[:128])
     check_distance(d, d64, delta, f"cfg1 distance {layout}")
+
+
+@pytest.mark.parametrize("kdop", [14, 18, 26])
+@pytest.mark.parametrize("Bf,bits", [(2, 4), (4, 8), (8, 16)])
+def test_config1_kdop(M, cfg1, kdop, Bf, bits):
+    # k-DOP bounding volumes on the static model B (Table I): band rule
+    # vs the oracle, the same counts as the AABB blob, and — the k-DOP is the
+    # AABB cut by more slabs, the descent rule sees only the AABB part — no
+    # more BV tests or leaf pairs than the AABB traversal
+    w, tA, tB, delta, cnt, H, Z = cfg1
+    A = build(M, w.A, Bf, bits)
+    Bb = build(M, w.B, Bf, bits)
+    Bk = build(M, w.B, Bf, bits, kdop=kdop)
+    h0, c0, s0 = run_collide(M, A, Bb, w.poses, stats=True)
+    hit, gc, sk = run_collide(M, A, Bk, w.poses, stats=True)
+    check_collide(hit, gc, H, Z, f"cfg1 k={kdop}")
+    assert np.array_equal(gc, c0)
+    assert sk["bv_tests"] <= s0["bv_tests"] and sk["leaf_pairs"] <= s0["leaf_pairs"]
+    d = run_distance(M, A, Bk, w.poses[:128])
+    d64, _ = O.distance(tA, tB, w.poses[:128])
+    check_distance(d, d64, delta, f"cfg1 distance k={kdop}")
+
+
+def test_kdop_on_moving_model_rejected(M, cfg1):
+    w = cfg1[0]
+    A = build(M, w.A, 4, 8, kdop=14)
+    B = build(M, w.B, 4, 8)
+    with pytest.raises(Exception, match="EINVAL"):
+        run_collide(M, A, B, w.poses[:4])
 
 
 def test_config1_early_exit(M, cfg1):
@@ -315,6 +345,21 @@ def test_config5_layouts_agree_full_size(M):
         if ref is None:
             ref = gc
         assert np.array_equal(gc, ref), layout
+
+
+def test_config5_kdop_full_size(M):
+    # full config 5 batch with 14- and 26-DOPs on B: the counts equal the
+    # AABB blob's on every pose, and a sample matches the oracle (band rule)
+    w = G.make_config(5)
+    A = build(M, w.A, w.branching, w.bits, w.treelet)
+    _, ref = run_collide(M, A, build(M, w.B, w.branching, w.bits, w.treelet), w.poses)
+    idx = _sample(len(w.poses), 200, 7)
+    tA, tB = oracle_trees(w)
+    _, H, Z, _ = O.collide(tA, tB, w.poses[idx], O.band_delta(w.A.vertices))
+    for k in (14, 26):
+        hit, gc = run_collide(M, A, build(M, w.B, w.branching, w.bits, w.treelet, kdop=k), w.poses)
+        assert np.array_equal(gc, ref), k
+        check_collide(hit[idx], gc[idx], H, Z, f"cfg5 k={k}")
 
 
 def test_config5_early_exit_full_size(M):
