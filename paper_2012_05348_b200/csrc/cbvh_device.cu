@@ -549,6 +549,67 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
   return m;
 }
 
+// Distance variant of the leaf refinement: per triangle of the leaf (mapped
+// into the box's frame as above) a lower bound on its distance to the box —
+// the larger of the gap between the box and the triangle's AABB and the gap
+// along the triangle's normal (separating axes: a lower bound on the distance
+// between the convex sets), less 2 eps.  Bit q: triangle q's bound is below
+// `best`; *lbmin = the smallest bound over the leaf's triangles.
+#ifndef CBVH_DIST_FILTER
+#define CBVH_DIST_FILTER 1
+#endif
+template <int DIR>
+__device__ CBVH_FILTER_ATTR uint32_t box_near_leaf(const PoseF& P, const float lo[3], const float hi[3],
+                                               const float* tris, uint32_t leaf, float eps, float best,
+                                               float* lbmin) {
+  const uint32_t first = leaf & 0x1FFFFFFFu, cnt = ((leaf >> 29) & 3u) + 1;
+  float c[3], h[3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
+  uint32_t m = 0;
+  float lbm = FLT_MAX;
+  TriRec next = load_rec(tris, first);
+  #pragma unroll 1
+  for (uint32_t q = 0; q < cnt; ++q) {
+    const TriRec cur = next;
+    if (q + 1 < cnt) next = load_rec(tris, first + q + 1);
+    const Tri L = rec_tri(cur);
+    float v[3][3];
+    #pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      if (DIR == 0) {
+        const float d0 = L.v[u][0] - P.t[0], d1 = L.v[u][1] - P.t[1], d2 = L.v[u][2] - P.t[2];
+        #pragma unroll
+        for (int k = 0; k < 3; ++k) v[u][k] = fmaf(P.R[0][k], d0, fmaf(P.R[1][k], d1, P.R[2][k] * d2)) - c[k];
+      } else {
+        #pragma unroll
+        for (int k = 0; k < 3; ++k)
+          v[u][k] = fmaf(P.R[k][0], L.v[u][0], fmaf(P.R[k][1], L.v[u][1], fmaf(P.R[k][2], L.v[u][2], P.t[k]))) - c[k];
+      }
+    }
+    float g2 = 0.f;
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float tlo = fminf(v[0][k], fminf(v[1][k], v[2][k]));
+      const float thi = fmaxf(v[0][k], fmaxf(v[1][k], v[2][k]));
+      const float g = fmaxf(0.f, fmaxf(tlo - h[k], -h[k] - thi));
+      g2 = fmaf(g, g, g2);
+    }
+    float e1[3], e2[3], n[3];
+    vsub(v[1], v[0], e1);
+    vsub(v[2], v[0], e2);
+    vcross(e1, e2, n);
+    const float nn = vdot(n, n);
+    const float rad_n = fmaf(fabsf(n[0]), h[0], fmaf(fabsf(n[1]), h[1], fabsf(n[2]) * h[2]));
+    const float gn = nn > 0.f ? (fabsf(vdot(n, v[0])) - rad_n) * rsqrtf(nn) : 0.f;
+    const float lb = fmaxf(sqrtf(g2), gn) - 2.f * eps;
+    if (lb < best) m |= 1u << q;
+    lbm = fminf(lbm, lb);
+  }
+  *lbmin = lbm;
+  return m;
+}
+
 #ifndef CBVH_DRAIN_INLINE
 #define CBVH_DRAIN_INLINE 1
 #endif
@@ -1237,6 +1298,22 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
             if (lb < best) lb = fmaxf(lb, kdop_gap<KX>(P, alo, ahi, p.X, CX, eps));
           }
           surv = lb < best;
+#if CBVH_DIST_FILTER
+          // against a leaf: per-triangle bounds (masks for the leaf phase, and
+          // a tighter pair bound)
+          if (surv && (ctb & kLeafBit)) {
+            float l2;
+            mskB = box_near_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps, best, &l2);
+            lb = fmaxf(lb, l2);
+            surv = mskB != 0u;
+          }
+          if (surv && (cta & kLeafBit)) {
+            float l2;
+            mskA = box_near_leaf<1>(P, blo, bhi, p.A.tris, cta, eps, best, &l2);
+            lb = fmaxf(lb, l2);
+            surv = mskA != 0u;
+          }
+#endif
         }
         if (STATS) {
           s_dec += (a_int ? 1 : 0) + (b_int ? 1 : 0);
