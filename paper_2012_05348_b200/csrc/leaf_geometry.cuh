@@ -142,22 +142,25 @@ __device__ __forceinline__ F pt_seg_d2(const F* p, const F* a, const F* b) {
   return vdot(q, q);
 }
 
-// min over (s,t) in [0,1]^2: the stationary point when inside, else the four
-// boundary point–segment distances; every candidate is a real pair of points,
-// so rounding can only over-estimate the minimum.
+// Segment–segment candidate: the stationary point of |p(s) - q(t)|^2 when it
+// lies inside [0,1]^2, else +inf.  A boundary minimum is an endpoint against
+// the other segment — a vertex–edge distance, which pt_tri_d2 already covers
+// (tri_tri_dist evaluates every vertex against every edge of the other
+// triangle), so only the interior candidate is needed here.  Every candidate
+// is a real pair of points, so rounding can only over-estimate the minimum.
 template <class F>
 __device__ F seg_seg_d2(const F* p0, const F* p1, const F* q0, const F* q1) {
-  F best = fmin(fmin(pt_seg_d2(p0, q0, q1), pt_seg_d2(p1, q0, q1)), fmin(pt_seg_d2(q0, p0, p1), pt_seg_d2(q1, p0, p1)));
   F d1[3], d2[3], r[3];
   vsub(p1, p0, d1); vsub(q1, q0, d2); vsub(p0, q0, r);
   F a = vdot(d1, d1), e = vdot(d2, d2), b = vdot(d1, d2), c = vdot(d1, r), f = vdot(d2, r);
   F den = a * e - b * b;
+  F best = F(FLT_MAX);
   if (den > 0) {
     const F inv = div_(F(1), den);
     F s = (b * f - c * e) * inv, t = (a * f - b * c) * inv;
     if (s >= 0 && s <= 1 && t >= 0 && t <= 1) {
       F w[3] = {r[0] + s * d1[0] - t * d2[0], r[1] + s * d1[1] - t * d2[1], r[2] + s * d1[2] - t * d2[2]};
-      best = fmin(best, vdot(w, w));
+      best = vdot(w, w);
     }
   }
   return best;
