@@ -167,12 +167,13 @@ __device__ F seg_seg_d2(const F* p0, const F* p1, const F* q0, const F* q1) {
 }
 
 // point–triangle: the plane distance when the projection lies inside the
-// closed triangle, else the nearest edge
+// closed triangle, else the nearest edge.  (With tri_tri_dist's interior-only
+// segment terms the minimum stays exact: a closest pair of two disjoint
+// triangles has a vertex of one of them, or two edge-interior points.)
 template <class F>
 __device__ F pt_tri_d2(const F* p, const TriT<F>& T) {
   F e1[3], e2[3], n[3], w[3];
   vsub(T.v[1], T.v[0], e1); vsub(T.v[2], T.v[0], e2); vcross(e1, e2, n);
-  F best = fmin(fmin(pt_seg_d2(p, T.v[0], T.v[1]), pt_seg_d2(p, T.v[1], T.v[2])), pt_seg_d2(p, T.v[2], T.v[0]));
   F nn = vdot(n, n);
   if (nn > 0) {
     vsub(p, T.v[0], w);
@@ -187,10 +188,10 @@ __device__ F pt_tri_d2(const F* p, const TriT<F>& T) {
     in = in && vdot(c0, n) >= 0;
     if (in) {
       F d = p[0] - q[0], e = p[1] - q[1], f = p[2] - q[2];
-      best = fmin(best, d * d + e * e + f * f);
+      return d * d + e * e + f * f;
     }
   }
-  return best;
+  return fmin(fmin(pt_seg_d2(p, T.v[0], T.v[1]), pt_seg_d2(p, T.v[1], T.v[2])), pt_seg_d2(p, T.v[2], T.v[0]));
 }
 
 template <class F>
