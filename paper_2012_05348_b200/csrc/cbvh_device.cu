@@ -351,16 +351,22 @@ __device__ __forceinline__ float sat_gap(const PoseF& P, const float alo[3], con
     gw[k] = fabsf(Tw[k]) - (hb[k] + ra);
     gmax = fmaxf(gmax, gw[k]);
   }
+  float ga[3];
   #pragma unroll
   for (int k = 0; k < 3; ++k) {
     float Ta = fmaf(P.R[0][k], Tw[0], fmaf(P.R[1][k], Tw[1], P.R[2][k] * Tw[2]));
     float rb = fmaf(fabsf(P.R[0][k]), hb[0], fmaf(fabsf(P.R[1][k]), hb[1], fabsf(P.R[2][k]) * hb[2]));
-    gmax = fmaxf(gmax, fabsf(Ta) - (ha[k] + rb));
+    ga[k] = fabsf(Ta) - (ha[k] + rb);
+    gmax = fmaxf(gmax, ga[k]);
   }
   if (WANT_LB) {
+    // Euclidean gaps: b against the world AABB of a, and a against the
+    // A-frame AABB of b (both contain the posed boxes)
     float g0 = fmaxf(gw[0], 0.f), g1 = fmaxf(gw[1], 0.f), g2 = fmaxf(gw[2], 0.f);
     float e = sqrtf(fmaf(g0, g0, fmaf(g1, g1, g2 * g2)));
-    *lb = fmaxf(fmaxf(e, gmax), 0.f) - eps;
+    g0 = fmaxf(ga[0], 0.f); g1 = fmaxf(ga[1], 0.f); g2 = fmaxf(ga[2], 0.f);
+    const float ea = sqrtf(fmaf(g0, g0, fmaf(g1, g1, g2 * g2)));
+    *lb = fmaxf(fmaxf(e, ea), 0.f) - eps;
   }
   return gmax - eps;
 }
