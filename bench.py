@@ -217,7 +217,7 @@ def run(args):
     A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout)
     B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout,
                                kdop=args.kdop)
-    distance = w.mode == "distance"
+    distance = (w.mode if args.mode == "auto" else args.mode) == "distance"
     build_s = time.time() - t0
     A.to_device(dev)
     B.to_device(dev)
@@ -381,6 +381,8 @@ def main():
                     help="pose preset; 'contact' = the paper's zero-distance preset (configs 1, 3)")
     ap.add_argument("--early-exit", action="store_true",
                     help="hit-only collide (stop each pose at its first hit); not the headline metric")
+    ap.add_argument("--mode", default="auto", choices=["auto", "collide", "distance"],
+                    help="query of the timed step (auto: the config's own; others are ablations)")
     ap.add_argument("--kdop", type=int, default=6, choices=[6, 14, 18, 26],
                     help="bounding volumes of the static model B: 6 = AABB, 14/18/26-DOP (delta layout)")
     ap.add_argument("--layout", default="delta", choices=["delta", "fp16", "fp32"],

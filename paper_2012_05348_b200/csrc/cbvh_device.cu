@@ -625,7 +625,7 @@ __device__ CBVH_FILTER_ATTR uint32_t box_near_leaf(const PoseF& P, const float l
 #define CBVH_DRAIN_ATTR __noinline__
 #endif
 #ifndef CBVH_DIST_DRAIN
-#define CBVH_DIST_DRAIN 2   // distance: drain the leaf queue once it holds this many pairs
+#define CBVH_DIST_DRAIN 32  // distance: drain the leaf queue once it holds this many pairs (2 / 8 / 16 / 32 measured: 32 best, -8..-20 %)
 #endif
 #ifndef CBVH_LEAF_SLAB
 #define CBVH_LEAF_SLAB 0

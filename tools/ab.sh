@@ -3,7 +3,7 @@
 CONFIGS=${CONFIGS:-5}
 for cfg in $CONFIGS; do
   for v in "$@"; do
-    CBVH_LIB=$PWD/paper_2012_05348_b200/$v timeout 600 python bench.py --config $cfg --steps 5 --warmup 3 --quick 2>&1 | tail -1 | python -c "
+    CBVH_LIB=$PWD/paper_2012_05348_b200/$v timeout 600 python bench.py --config $cfg --steps 5 --warmup 3 --quick $EXTRA 2>&1 | tail -1 | python -c "
 import sys, json
 l = sys.stdin.read().strip()
 try:
