@@ -1384,8 +1384,9 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
         }
       }
       __syncwarp();
-      // collide: drain in full rounds; distance: drain promptly so that the
-      // pose's best distance tightens and prunes the rest of the traversal
+      // drain in full rounds (collide above 32 entries, distance at
+      // CBVH_DIST_DRAIN: a sooner drain tightens a pose's best earlier, but
+      // the half-empty rounds cost more than the pruning gains)
       if (nleaf > kLeafQ - 32 || (MODE == 1 && nleaf >= CBVH_DIST_DRAIN)) {
         s_tri += drain_leaves<MODE>(p, c, nleaf);
         nleaf = 0;
