@@ -454,12 +454,17 @@ __device__ __forceinline__ bool tri_boxes_overlap(const Tri& V, const Tri& U) {
 #ifndef CBVH_TRIBOX_EDGES
 #define CBVH_TRIBOX_EDGES 0
 #endif
+// the leaf filter maps triangles straight to box-centred coordinates (the
+// pose offset and the box centre folded into one FMA chain per coordinate)
+#ifndef CBVH_FOLD_CENTRE
+#define CBVH_FOLD_CENTRE 1
+#endif
 __device__ __forceinline__ bool box_tri_overlap(const float c[3], const float h[3], const Tri& T, float eps) {
   float v[3][3];
   #pragma unroll
   for (int q = 0; q < 3; ++q)
     #pragma unroll
-    for (int k = 0; k < 3; ++k) v[q][k] = T.v[q][k] - c[k];  // box-centred
+    for (int k = 0; k < 3; ++k) v[q][k] = CBVH_FOLD_CENTRE ? T.v[q][k] : T.v[q][k] - c[k];  // box-centred
   #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const float tlo = fminf(v[0][k], fminf(v[1][k], v[2][k]));
@@ -533,6 +538,12 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
   float c[3], h[3];
   #pragma unroll
   for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
+#if CBVH_FOLD_CENTRE
+  float off[3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k)
+    off[k] = DIR == 0 ? -fmaf(P.R[0][k], P.t[0], fmaf(P.R[1][k], P.t[1], fmaf(P.R[2][k], P.t[2], c[k]))) : P.t[k] - c[k];
+#endif
   uint32_t m = 0;
   TriRec next = load_rec(tris, first);
   #pragma unroll 1
@@ -541,6 +552,16 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
     if (q + 1 < cnt) next = load_rec(tris, first + q + 1);
     const Tri L = rec_tri(cur);
     Tri W;
+#if CBVH_FOLD_CENTRE
+    // DIR 0: w = R^T v - (R^T t + c); DIR 1: w = R v + (t - c) — the filter
+    // is conservative by eps, which covers the rounding of the folded offset
+    #pragma unroll
+    for (int v = 0; v < 3; ++v)
+      #pragma unroll
+      for (int k = 0; k < 3; ++k)
+        W.v[v][k] = DIR == 0 ? fmaf(P.R[0][k], L.v[v][0], fmaf(P.R[1][k], L.v[v][1], fmaf(P.R[2][k], L.v[v][2], off[k])))
+                             : fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], off[k])));
+#else
     if (DIR == 0) {
       W = to_local(P, L);
     } else {
@@ -550,6 +571,7 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
         for (int k = 0; k < 3; ++k)
           W.v[v][k] = fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], P.t[k])));
     }
+#endif
     if (box_tri_overlap(c, h, W, eps)) m |= 1u << q;
   }
   return m;
@@ -763,7 +785,9 @@ __device__ __forceinline__ uint32_t descent_flags(int rule, uint32_t ta, uint32_
 // (k + 1/2) / d is at least 1/(2d) away from the next integer, far above the
 // ~1e-6 relative error of the fp32 reciprocal.
 __device__ __forceinline__ int small_div(int k, int d) {
-  return __float2int_rz(((float)k + 0.5f) * __frcp_rn((float)d));
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)d));  // one MUFU, ~1 ulp
+  return __float2int_rz(((float)k + 0.5f) * r);
 }
 
 // all triangles of a leaf: low (ntri) bits set
