@@ -384,3 +384,67 @@ def test_config5_full_size_sampled(M):
     _, H, Z, _ = O.collide(tA, tB, w.poses[idx], delta)
     rep = check_collide(hit[idx], gc[idx], H, Z, "cfg5")
     print("cfg5", rep)
+
+
+_PHASE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2012_05348_b200 as M
+from workloads import generators as G
+w = G.make_config(3, num_poses=65536)
+A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet).to_device()
+B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet).to_device()
+P = torch.from_numpy(w.poses).cuda()
+ws = M.Workspace(A, B, 0)
+hit, cnt = M.collide_batch(A, B, P, workspace=ws, stats=True)
+M.check(ws)
+st = M.read_stats(ws)
+wd = M.Workspace(A, B, 1)
+d = M.distance_batch(A, B, P[:4096], workspace=wd)
+M.check(wd)
+np.savez({out!r}, cnt=cnt.cpu().numpy().view(np.uint32), d=d.cpu().numpy(), dumped=st["dumped"])
+"""
+
+
+@pytest.mark.parametrize("phases", ["0", "1,1,1,1,1,1", "4,0,2", "1000000"])
+def test_load_balancing_phases_do_not_change_results(M, tmp_path, phases):
+    # the continuation phases (DESIGN §4.5) only move work between warps and
+    # launches: any budget schedule (immediate dumps, many tiny phases, one
+    # unbounded phase) gives the default schedule's counts and distances
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for tag, env in (("default", None), ("variant", phases)):
+        out = str(tmp_path / f"{tag}.npz")
+        e = dict(os.environ)
+        e.pop("CBVH_PHASES", None)
+        if env is not None:
+            e["CBVH_PHASES"] = env
+        subprocess.run([sys.executable, "-c", _PHASE_SCRIPT.format(root=root, out=out)], env=e, check=True,
+                       timeout=600)
+        res[tag] = np.load(out)
+    assert np.array_equal(res["default"]["cnt"], res["variant"]["cnt"])
+    assert np.array_equal(res["default"]["d"], res["variant"]["d"])
+    if phases in ("0", "1,1,1,1,1,1"):
+        assert int(res["variant"]["dumped"]) > 0  # the schedule really moved work between launches
+
+
+def test_config5_4x_poses_sampled(M):
+    # 4,194,304 poses in one call (4x the headline batch): hit == (count > 0)
+    # everywhere, the first 1M poses equal the 1M-pose call, and a sample of
+    # the extra poses matches the oracle
+    w = G.make_config(5)
+    w4 = G.make_config(5, num_poses=4 * len(w.poses), pose_seed_offset=11)
+    P = np.concatenate([w.poses, w4.poses[len(w.poses):]])
+    A = build(M, w.A, w.branching, w.bits, w.treelet)
+    B = build(M, w.B, w.branching, w.bits, w.treelet)
+    hit, gc = run_collide(M, A, B, P)
+    assert np.array_equal(hit == 1, gc > 0)
+    _, ref = run_collide(M, A, B, w.poses)
+    assert np.array_equal(gc[:len(w.poses)], ref)
+    idx = len(w.poses) + _sample(len(P) - len(w.poses), 150, 9)
+    tA, tB = oracle_trees(w)
+    _, H, Z, _ = O.collide(tA, tB, P[idx], O.band_delta(w.A.vertices))
+    check_collide(hit[idx], gc[idx], H, Z, "cfg5 x4")
