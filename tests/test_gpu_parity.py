@@ -448,3 +448,34 @@ def test_config5_4x_poses_sampled(M):
     tA, tB = oracle_trees(w)
     _, H, Z, _ = O.collide(tA, tB, P[idx], O.band_delta(w.A.vertices))
     check_collide(hit[idx], gc[idx], H, Z, "cfg5 x4")
+
+
+def test_concurrent_streams_distinct_workspaces(M, cfg1):
+    # include/cbvh.h: blobs are immutable; calls on different streams with
+    # distinct workspaces may run concurrently
+    w = cfg1[0]
+    A, B = build(M, w.A, 4, 8), build(M, w.B, 4, 8)
+    P1 = torch.from_numpy(np.ascontiguousarray(w.poses[:512])).cuda()
+    P2 = torch.from_numpy(np.ascontiguousarray(w.poses[512:])).cuda()
+    ref_hit, ref_cnt = run_collide(M, A, B, w.poses)
+    ref_d = run_distance(M, A, B, w.poses[:256])
+    s1, s2, s3 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    ws1, ws2, ws3 = M.Workspace(A, B, 0), M.Workspace(A, B, 0), M.Workspace(A, B, 1)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            h1, c1 = M.collide_batch(A, B, P1, workspace=ws1, stream=s1)
+        with torch.cuda.stream(s2):
+            h2, c2 = M.collide_batch(A, B, P2, workspace=ws2, stream=s2)
+        with torch.cuda.stream(s3):
+            d3 = M.distance_batch(A, B, P1[:256], workspace=ws3, stream=s3)
+        M.check(ws1, s1)
+        M.check(ws2, s2)
+        M.check(ws3, s3)
+        torch.cuda.synchronize()
+        cnt = np.concatenate([c1.cpu().numpy(), c2.cpu().numpy()]).view(np.uint32).astype(np.int64)
+        hit = np.concatenate([h1.cpu().numpy(), h2.cpu().numpy()])
+        assert np.array_equal(cnt, ref_cnt) and np.array_equal(hit, ref_hit)
+        # (the visiting order may differ between runs; the minimum agrees to
+        # fp32 rounding of near-tied candidates)
+        assert np.allclose(d3.cpu().numpy(), ref_d, rtol=1e-6, atol=0)
