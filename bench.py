@@ -283,7 +283,7 @@ def run(args):
                               "dumped": st["dumped"], "launches": M.last_launch_count(),
                               "timeline_ms": [t / 1e6 for t in st["timeline_ns"]],
                               "lane_util": st["bv_tests"] / max(1, 32 * st["iterations"]),
-                              "iterations": st["iterations"], "bv_tests": st["bv_tests"], "leaf_pairs": st["leaf_pairs"], "tri_tests": st["tri_tests"], "layout": args.layout, "kdop": args.kdop, "early_exit": args.early_exit,
+                              "iterations": st["iterations"], "bv_tests": st["bv_tests"], "leaf_pairs": st["leaf_pairs"], "tri_tests": st["tri_tests"], "exact_tests": st["exact_tests"], "layout": args.layout, "kdop": args.kdop, "early_exit": args.early_exit,
                               "bytes_per_node": {"A": A.info["bytes_per_node"], "B": B.info["bytes_per_node"]}}), flush=True)
         return
 

@@ -200,6 +200,7 @@ typedef struct {
   uint64_t dumped;          /* items handed to a later load-balancing phase (continuations) */
   uint64_t timeline_ns[8];  /* when the pose cursor passed k/8 of N (ns after the kernel start) */
   uint64_t iterations;      /* warp expansion passes; bv_tests / (32 x iterations) = lane utilisation */
+  uint64_t exact_tests;     /* triangle pairs past the leaf phase's cheap culls: exact Möller / distance evaluations */
 } cbvh_stats;
 
 /* Same as collide_batch / distance_batch but also accumulate cbvh_stats in

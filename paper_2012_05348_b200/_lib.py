@@ -59,7 +59,7 @@ class cbvh_stats(C.Structure):
                 ("tri_tests", C.c_uint64), ("nodes_decoded", C.c_uint64), ("record_bytes", C.c_uint64),
                 ("tri_bytes", C.c_uint64), ("spills", C.c_uint64), ("kernel_ns", C.c_uint64),
                 ("tail_ns", C.c_uint64), ("dumped", C.c_uint64), ("timeline_ns", C.c_uint64 * 8),
-                ("iterations", C.c_uint64)]
+                ("iterations", C.c_uint64), ("exact_tests", C.c_uint64)]
 
 
 class cbvh_query_opts(C.Structure):

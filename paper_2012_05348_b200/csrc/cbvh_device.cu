@@ -84,6 +84,7 @@ struct Control {
   unsigned long long stats[8];
   unsigned long long t_frac[8];  // stats variant: when the pose cursor passed k/8 of N
   unsigned long long iterations; // stats variant: expansion passes (warp iterations)
+  unsigned long long exact;      // stats variant: triangle pairs past the culls (exact Möller / distance)
 };
 static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte workspace header");
 
@@ -327,6 +328,15 @@ __device__ __forceinline__ PoseF load_pose(const float* poses, int i) {
 
 // ---------------------------------------------------------------- BV test
 
+#ifndef CBVH_DIST_CAXIS
+#define CBVH_DIST_CAXIS 1
+#endif
+#ifndef CBVH_DIST_LAXIS
+#define CBVH_DIST_LAXIS 1
+#endif
+#ifndef CBVH_SAT_EDGES
+#define CBVH_SAT_EDGES 0
+#endif
 // SAT between box a (A-local, under pose P) and box b (world).  Returns the
 // largest separating gap over the 6 axes (> 0 means separated) and, for the
 // distance variant, the exact gap between b and the world AABB of a.
@@ -351,14 +361,35 @@ __device__ __forceinline__ float sat_gap(const PoseF& P, const float alo[3], con
     gw[k] = fabsf(Tw[k]) - (hb[k] + ra);
     gmax = fmaxf(gmax, gw[k]);
   }
-  float ga[3];
+  float ga[3], Ta[3];
   #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    float Ta = fmaf(P.R[0][k], Tw[0], fmaf(P.R[1][k], Tw[1], P.R[2][k] * Tw[2]));
+    Ta[k] = fmaf(P.R[0][k], Tw[0], fmaf(P.R[1][k], Tw[1], P.R[2][k] * Tw[2]));
     float rb = fmaf(fabsf(P.R[0][k]), hb[0], fmaf(fabsf(P.R[1][k]), hb[1], fabsf(P.R[2][k]) * hb[2]));
-    ga[k] = fabsf(Ta) - (ha[k] + rb);
+    ga[k] = fabsf(Ta[k]) - (ha[k] + rb);
     gmax = fmaxf(gmax, ga[k]);
   }
+#if CBVH_SAT_EDGES
+  if (!WANT_LB && gmax <= eps) {
+    // the 9 edge axes L = A_i x e_j (Gottschalk's OBB test): A's
+    // columns are orthonormal up to ~1e-7, so A's radius on L uses
+    // A_k x A_i = +-A_m; the unnormalised gap (|L| <= 1) is compared with eps
+    #pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int i1 = (i + 1) % 3, i2 = (i + 2) % 3;
+      #pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+        // L = A_i x e_j: L[j] = 0, L[j1] = A_i[j2], L[j2] = -A_i[j1]
+        const float l1 = P.R[j2][i], l2 = -P.R[j1][i];
+        const float tl = fmaf(Tw[j1], l1, Tw[j2] * l2);
+        const float ra = fmaf(ha[i1], fabsf(P.R[j][i2]), ha[i2] * fabsf(P.R[j][i1]));
+        const float rb = fmaf(hb[j1], fabsf(l1), hb[j2] * fabsf(l2));
+        gmax = fmaxf(gmax, fabsf(tl) - (ra + rb));
+      }
+    }
+  }
+#endif
   if (WANT_LB) {
     // Euclidean gaps: b against the world AABB of a, and a against the
     // A-frame AABB of b (both contain the posed boxes)
@@ -366,7 +397,18 @@ __device__ __forceinline__ float sat_gap(const PoseF& P, const float alo[3], con
     float e = sqrtf(fmaf(g0, g0, fmaf(g1, g1, g2 * g2)));
     g0 = fmaxf(ga[0], 0.f); g1 = fmaxf(ga[1], 0.f); g2 = fmaxf(ga[2], 0.f);
     const float ea = sqrtf(fmaf(g0, g0, fmaf(g1, g1, g2 * g2)));
+#if CBVH_DIST_CAXIS
+    // the axis through the two box centres, u = Tw / |Tw|: |Tw| less the
+    // radii of both boxes on u (A's from Ta = R^T Tw) — for boxes far apart
+    // relative to their size this is nearly the true distance
+    const float T2 = fmaf(Tw[0], Tw[0], fmaf(Tw[1], Tw[1], Tw[2] * Tw[2]));
+    const float rs = fmaf(ha[0], fabsf(Ta[0]), fmaf(ha[1], fabsf(Ta[1]), fmaf(ha[2], fabsf(Ta[2]),
+                     fmaf(hb[0], fabsf(Tw[0]), fmaf(hb[1], fabsf(Tw[1]), hb[2] * fabsf(Tw[2]))))));
+    const float ec = T2 > 0.f ? (T2 - rs) * rsqrtf(T2) : 0.f;
+    *lb = fmaxf(fmaxf(fmaxf(e, ea), ec), 0.f) - eps;
+#else
     *lb = fmaxf(fmaxf(e, ea), 0.f) - eps;
+#endif
   }
   return gmax - eps;
 }
@@ -531,10 +573,14 @@ __device__ __forceinline__ Tri rec_tri(const TriRec& r) {
 #else
 #define CBVH_FILTER_ATTR __noinline__
 #endif
+// Only the triangles in `todo` are tested: a triangle the parent box missed
+// cannot touch the child box (child ⊆ parent, same eps), so the mask an item
+// inherits from its parent's refinement is a valid starting set.
 template <int DIR>
 __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float lo[3], const float hi[3],
-                                               const float* tris, uint32_t leaf, float eps) {
-  const uint32_t first = leaf & 0x1FFFFFFFu, cnt = ((leaf >> 29) & 3u) + 1;
+                                               const float* tris, uint32_t leaf, float eps, uint32_t todo) {
+  const uint32_t first = leaf & 0x1FFFFFFFu;
+  todo &= (2u << ((leaf >> 29) & 3u)) - 1u;
   float c[3], h[3];
   #pragma unroll
   for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
@@ -545,11 +591,20 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
     off[k] = DIR == 0 ? -fmaf(P.R[0][k], P.t[0], fmaf(P.R[1][k], P.t[1], fmaf(P.R[2][k], P.t[2], c[k]))) : P.t[k] - c[k];
 #endif
   uint32_t m = 0;
-  TriRec next = load_rec(tris, first);
+  if (todo == 0u) return 0u;
+  uint32_t qn = (uint32_t)__ffs(todo) - 1u;
+  todo &= todo - 1u;
+  TriRec next = load_rec(tris, first + qn);
   #pragma unroll 1
-  for (uint32_t q = 0; q < cnt; ++q) {
+  while (true) {
     const TriRec cur = next;
-    if (q + 1 < cnt) next = load_rec(tris, first + q + 1);
+    const uint32_t q = qn;
+    const bool more = todo != 0u;
+    if (more) {
+      qn = (uint32_t)__ffs(todo) - 1u;
+      todo &= todo - 1u;
+      next = load_rec(tris, first + qn);
+    }
     const Tri L = rec_tri(cur);
     Tri W;
 #if CBVH_FOLD_CENTRE
@@ -573,6 +628,7 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
     }
 #endif
     if (box_tri_overlap(c, h, W, eps)) m |= 1u << q;
+    if (!more) break;
   }
   return m;
 }
@@ -583,6 +639,11 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
 // along the triangle's normal (separating axes: a lower bound on the distance
 // between the convex sets), less 2 eps.  Bit q: triangle q's bound is below
 // `best`; *lbmin = the smallest bound over the leaf's triangles.
+// collide: an item carries the leaf-triangle masks of its refinement, so a
+// child box is tested only against the triangles its parent box touched
+#ifndef CBVH_MASK_PROP
+#define CBVH_MASK_PROP 1
+#endif
 #ifndef CBVH_DIST_FILTER
 #define CBVH_DIST_FILTER 1
 #endif
@@ -630,7 +691,20 @@ __device__ CBVH_FILTER_ATTR uint32_t box_near_leaf(const PoseF& P, const float l
     const float nn = vdot(n, n);
     const float rad_n = fmaf(fabsf(n[0]), h[0], fmaf(fabsf(n[1]), h[1], fabsf(n[2]) * h[2]));
     const float gn = nn > 0.f ? (fabsf(vdot(n, v[0])) - rad_n) * rsqrtf(nn) : 0.f;
+#if CBVH_DIST_LAXIS
+    // the axis from the box centre (the origin here) to the triangle's
+    // centroid: the triangle's nearest projection less the box radius
+    float ct[3];
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) ct[k] = (v[0][k] + v[1][k] + v[2][k]) * (1.f / 3.f);
+    const float c2 = fmaf(ct[0], ct[0], fmaf(ct[1], ct[1], ct[2] * ct[2]));
+    const float pmin = fminf(vdot(ct, v[0]), fminf(vdot(ct, v[1]), vdot(ct, v[2])));
+    const float rb = fmaf(fabsf(ct[0]), h[0], fmaf(fabsf(ct[1]), h[1], fabsf(ct[2]) * h[2]));
+    const float gc = c2 > 0.f ? (pmin - rb) * rsqrtf(c2) : 0.f;
+    const float lb = fmaxf(fmaxf(sqrtf(g2), gn), gc) - 2.f * eps;
+#else
     const float lb = fmaxf(sqrtf(g2), gn) - 2.f * eps;
+#endif
     if (lb < best) m |= 1u << q;
     lbm = fminf(lbm, lb);
   }
@@ -727,6 +801,32 @@ __device__ __forceinline__ float tri_box_gap(const Tri& V, const Tri& U) {
     g2 = fmaf(g, g, g2);
   }
   return sqrtf(g2);
+}
+
+// Gap between two triangles along the line through their centroids (a
+// separating-axis lower bound on their distance; for small triangles far
+// apart it is within ~size^2 / distance of the true distance, where the AABB
+// gap is off by ~size x tilt).  Projections are taken relative to V's
+// centroid so the magnitudes stay small.
+#ifndef CBVH_DIST_AXIS
+#define CBVH_DIST_AXIS 1
+#endif
+__device__ __forceinline__ float tri_axis_gap(const Tri& V, const Tri& U) {
+  float cv[3], u[3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    cv[k] = (V.v[0][k] + V.v[1][k] + V.v[2][k]) * (1.f / 3.f);
+    u[k] = (U.v[0][k] + U.v[1][k] + U.v[2][k]) * (1.f / 3.f) - cv[k];
+  }
+  const float L2 = fmaf(u[0], u[0], fmaf(u[1], u[1], u[2] * u[2]));
+  if (!(L2 > 0.f)) return 0.f;
+  float vmax = -FLT_MAX, umin = FLT_MAX;
+  #pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    vmax = fmaxf(vmax, fmaf(u[0], V.v[q][0] - cv[0], fmaf(u[1], V.v[q][1] - cv[1], u[2] * (V.v[q][2] - cv[2]))));
+    umin = fminf(umin, fmaf(u[0], U.v[q][0] - cv[0], fmaf(u[1], U.v[q][1] - cv[1], u[2] * (U.v[q][2] - cv[2]))));
+  }
+  return (umin - vmax) * rsqrtf(L2);
 }
 
 // fp64 re-evaluation of a near-contact distance candidate,
@@ -864,8 +964,9 @@ __device__ __forceinline__ void exact_batch(const Params& p, const WarpCtx c, in
 // expensive tests 32 at a time, so Möller / the distance code run with full
 // lanes instead of the ~20-30 % the culls leave.  Returns the number of
 // triangle-pair tests (stats).
-template <int MODE>
-__device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx c, int nleaf) {
+template <int MODE, bool STATS>
+__device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx c, int nleaf,
+                                                 unsigned long long* exact) {
   unsigned tests = 0;
   int head = 0, nsq = 0;
   const unsigned lt = lanemask_lt();
@@ -935,12 +1036,19 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
         // triangles whose AABBs are disjoint cannot intersect.  Collide runs
         // Möller in place (measured: the compaction costs more than the
         // ~30 % SIMT it recovers for this cheaper test).
-        hit = tri_boxes_overlap(TA, TB) && tri_tri_overlap(TA, TB);
+        const bool cand = tri_boxes_overlap(TA, TB);
+        if (STATS && cand) ++*exact;
+        hit = cand && tri_tri_overlap(TA, TB);
       } else {
         // triangle AABB gap: a lower bound; skip pairs that cannot beat the best
         const float tmax0 = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
         const float best = __uint_as_float(__ldcg(&p.dist_bits[my_pose]));
-        keep = tri_box_gap(TA, TB) - 2e-6f * (tmax0 + p.A.maxabs + p.B.maxabs) < best;
+        const float slack = 2e-6f * (tmax0 + p.A.maxabs + p.B.maxabs);
+        keep = tri_box_gap(TA, TB) - slack < best;
+#if CBVH_DIST_AXIS
+        if (keep) keep = tri_axis_gap(TA, TB) - slack < best;
+#endif
+        if (STATS && keep) ++*exact;
       }
     }
     tests += (unsigned)total;
@@ -1089,7 +1197,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * NF;
   int top = 0, nleaf = 0, spill_top = 0;
   int after = 0;  // iterations since the input ran out
-  unsigned long long s_dump = 0, s_iter = 0;
+  unsigned long long s_dump = 0, s_iter = 0, s_exact = 0;
   unsigned long long s_bv = 0, s_exp = 0, s_leaf = 0, s_tri = 0, s_dec = 0, s_rec = 0, s_lbytes = 0, s_spill = 0;
   bool poses_left = true;
   const unsigned lt = lanemask_lt();
@@ -1144,13 +1252,13 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
               }
               #pragma unroll
               for (int q = 0; q < 2 * KX; ++q) c.st[(F_XB + q) * kStack + slot] = (uint32_t)p.X.root[q];
-              c.st[F_LB * kStack + slot] = 0u;
+              c.st[F_LB * kStack + slot] = MODE == 0 ? 0xFFu : 0u;  // collide: inherited leaf masks (all)
             }
           }
           if (root_leafpair) nleaf += k; else top += k;
           __syncwarp();
           if (nleaf > kLeafQ - 32) {
-            s_tri += drain_leaves<MODE>(p, c, nleaf);
+            s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
             nleaf = 0;
           }
         }
@@ -1185,7 +1293,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     // ---- bounded work after the input ran out: hand the rest to the next phase
     if (!poses_left && p.budget >= 0 && ++after > p.budget) {
       if (nleaf > 0) {
-        s_tri += drain_leaves<MODE>(p, c, nleaf);
+        s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
         nleaf = 0;
       }
       if (dump_items<NF>(p, c, top, spill_top)) {
@@ -1237,7 +1345,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     }
     #pragma unroll
     for (int q = 0; q < 2 * KX; ++q) BX[q] = (int32_t)c.st[(F_XB + q) * kStack + slot];
-    const float item_lb = __uint_as_float(c.st[F_LB * kStack + slot]);
+    const uint32_t item_w = c.st[F_LB * kStack + slot];  // distance: lower bound; collide: leaf masks
+    const float item_lb = __uint_as_float(item_w);
     __syncwarp();
     top -= m;
     if (STATS) { s_exp += m; s_iter += passes; }
@@ -1262,7 +1371,13 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       uint32_t cta = ta, ctb = tb;
       bool surv = false;
       float lb = 0.f;
+      // triangles of a leaf side the parent's refinement kept (collide; a
+      // descended side is a new node: all)
       uint32_t mskA = 15u, mskB = 15u;
+      if (MODE == 0 && CBVH_MASK_PROP) {
+        if (!a_int) mskA = item_w & 15u;
+        if (!b_int) mskB = (item_w >> 4) & 15u;
+      }
       bool bad = false;  // checked build: an out-of-range child drops the lane
       if (valid) {
         if (a_int) {
@@ -1315,11 +1430,11 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
           const bool doB = lbf, doA = la;
 #endif
           if (surv && doB) {
-            mskB = box_hits_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps);
+            mskB = box_hits_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps, mskB);
             surv = mskB != 0u;
           }
           if (surv && doA) {
-            mskA = box_hits_leaf<1>(P, blo, bhi, p.A.tris, cta, eps);
+            mskA = box_hits_leaf<1>(P, blo, bhi, p.A.tris, cta, eps, mskA);
             surv = mskA != 0u;
           }
         } else {
@@ -1386,6 +1501,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
           #pragma unroll
           for (int q = 0; q < 2 * KX; ++q) c.st[(F_XB + q) * kStack + s2] = (uint32_t)CX[q];
           if (MODE == 1) c.st[F_LB * kStack + s2] = __float_as_uint(lb);
+          else c.st[F_LB * kStack + s2] = (mskA & 15u) | ((mskB & 15u) << 4);
         }
         top += __popc(pm);
       }
@@ -1412,21 +1528,22 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       // CBVH_DIST_DRAIN: a sooner drain tightens a pose's best earlier, but
       // the half-empty rounds cost more than the pruning gains)
       if (nleaf > kLeafQ - 32 || (MODE == 1 && nleaf >= CBVH_DIST_DRAIN)) {
-        s_tri += drain_leaves<MODE>(p, c, nleaf);
+        s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
         nleaf = 0;
       }
     }
     if (MODE == 1 && nleaf > 0 && top == 0) {
-      s_tri += drain_leaves<MODE>(p, c, nleaf);
+      s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
       nleaf = 0;
     }
   }
-  if (nleaf > 0) s_tri += drain_leaves<MODE>(p, c, nleaf);
+  if (nleaf > 0) s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
   if (STATS && c.lane == 0) atomicMax(&p.ctl->t_end, globaltimer_ns());
   if (STATS) {
-    unsigned long long d = s_dec, r = s_rec, lb = s_lbytes;
+    unsigned long long d = s_dec, r = s_rec, lb = s_lbytes, ex = s_exact;
     #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
+      ex += __shfl_down_sync(FULL, ex, o);
       d += __shfl_down_sync(FULL, d, o);
       r += __shfl_down_sync(FULL, r, o);
       lb += __shfl_down_sync(FULL, lb, o);
@@ -1442,6 +1559,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       atomicAdd(&p.ctl->stats[7], s_spill);
       atomicAdd(&p.ctl->dumped, s_dump);
       atomicAdd(&p.ctl->iterations, s_iter);
+      atomicAdd(&p.ctl->exact, ex);
     }
   }
 }
@@ -1467,6 +1585,7 @@ __global__ void init_kernel(Params p, int reset_stats) {
       p.ctl->t_end = 0ull;
       p.ctl->dumped = 0ull;
       p.ctl->iterations = 0ull;
+      p.ctl->exact = 0ull;
       for (int s = 0; s < 8; ++s) p.ctl->t_frac[s] = ~0ull;
     }
   }
@@ -1861,6 +1980,7 @@ int cbvh_read_stats(const void* d_ws, cbvh_stats* out, void* stream) {
   out->tail_ns = (timed && ctl.t_exhausted != ~0ull && ctl.t_end >= ctl.t_exhausted) ? ctl.t_end - ctl.t_exhausted : 0;
   out->dumped = ctl.dumped;
   out->iterations = ctl.iterations;
+  out->exact_tests = ctl.exact;
   for (int k = 0; k < 8; ++k)
     out->timeline_ns[k] = (timed && ctl.t_frac[k] != ~0ull && ctl.t_frac[k] >= ctl.t_start) ? ctl.t_frac[k] - ctl.t_start : 0;
   return CBVH_OK;

@@ -7,7 +7,7 @@ for cfg in $CONFIGS; do
 import sys, json
 l = sys.stdin.read().strip()
 try:
-    d = json.loads(l); print('cfg$cfg', '$v', round(d['ms_per_step'], 3), 'ms', round(d['value'] / 1e6, 3), 'M/s', 'lane_util', round(d.get('lane_util', 0), 3), 'iters', d.get('iterations'), 'bv', d.get('bv_tests'), 'leaf', d.get('leaf_pairs'), 'tri', d.get('tri_tests'))
+    d = json.loads(l); print('cfg$cfg', '$v', round(d['ms_per_step'], 3), 'ms', round(d['value'] / 1e6, 3), 'M/s', 'lane_util', round(d.get('lane_util', 0), 3), 'iters', d.get('iterations'), 'bv', d.get('bv_tests'), 'leaf', d.get('leaf_pairs'), 'tri', d.get('tri_tests'), 'exact', d.get('exact_tests'))
 except Exception:
     print('cfg$cfg', '$v', 'FAILED', l[-300:])
 "
