@@ -175,6 +175,12 @@ typedef struct {
   int stats;      /* non-zero: accumulate cbvh_stats in the workspace (slower) */
   int early_exit; /* collide only: stop each pose at its first colliding pair ("early_exit").
                      d_hit stays exact; d_pair_count becomes a lower bound (>= 1 iff hit). */
+  int capped;     /* distance only: on entry d_min_dist[i] holds a cap c_i (e.g. a clearance
+                     threshold or the previous frame's distance); on return d_min_dist[i] =
+                     min(distance_i, c_i), exact whenever distance_i < c_i.  Node pairs whose
+                     lower bound reaches the cap are pruned from the start (S:397-405 prune
+                     rule with best initialised to c_i instead of +inf).  NaN caps act as
+                     +inf, negative caps as 0.  Ignored by collide. */
 } cbvh_query_opts;
 
 /* collide_batch / distance_batch with options (opts may be null). */

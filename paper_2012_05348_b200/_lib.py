@@ -63,7 +63,7 @@ class cbvh_stats(C.Structure):
 
 
 class cbvh_query_opts(C.Structure):
-    _fields_ = [("descent", C.c_int), ("stats", C.c_int), ("early_exit", C.c_int)]
+    _fields_ = [("descent", C.c_int), ("stats", C.c_int), ("early_exit", C.c_int), ("capped", C.c_int)]
 
 
 CBVH_DESCENT_SIMULTANEOUS, CBVH_DESCENT_LARGER = 0, 1

@@ -137,10 +137,10 @@ def validate_poses(poses, tol: float = 1e-6) -> np.ndarray:
     return np.nonzero(bad)[0]
 
 
-def _opts(descent: str, stats: bool, early_exit: bool = False) -> L.cbvh_query_opts:
+def _opts(descent: str, stats: bool, early_exit: bool = False, capped: bool = False) -> L.cbvh_query_opts:
     if descent not in L.DESCENT:
         raise ValueError(f"descent must be one of {sorted(L.DESCENT)}")
-    return L.cbvh_query_opts(L.DESCENT[descent], 1 if stats else 0, 1 if early_exit else 0)
+    return L.cbvh_query_opts(L.DESCENT[descent], 1 if stats else 0, 1 if early_exit else 0, 1 if capped else 0)
 
 
 def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=None,
@@ -171,15 +171,21 @@ def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=Non
 
 def distance_batch(A: CompressedBVH, B: CompressedBVH, poses, dist=None,
                    workspace: Workspace | None = None, stream=None, stats: bool = False,
-                   descent: str = "larger"):
-    """C-ABI distance_batch: per-pose minimum triangle–triangle distance (fp32)."""
+                   descent: str = "larger", caps=None):
+    """C-ABI distance_batch: per-pose minimum triangle–triangle distance (fp32).
+    caps (optional, fp32 [N] on the poses' device): per-pose caps — the result
+    is min(distance, cap), exact below the cap (cbvh_query_opts.capped)."""
     torch = _torch()
     N = _check_poses(poses)
     if dist is None:
         dist = torch.empty(N, dtype=torch.float32, device=poses.device)
+    if caps is not None:
+        if caps.shape != (N,) or caps.dtype != torch.float32 or caps.device != poses.device:
+            raise ValueError("caps must be fp32 [N] on the poses' device")
+        dist.copy_(caps)
     if workspace is None:
         workspace = Workspace(A, B, 1, poses.device)
-    o = _opts(descent, stats)
+    o = _opts(descent, stats, capped=caps is not None)
     L.check(L.load().distance_batch_ex(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
                                        C.c_void_p(dist.data_ptr()), C.c_void_p(workspace.ptr), workspace.nbytes,
                                        C.c_void_p(_stream_ptr(stream)), C.byref(o)))

@@ -138,6 +138,7 @@ struct Params {
   int budget;            // iterations a warp may run after its input is exhausted (< 0: unbounded)
   int descent;           // CBVH_DESCENT_SIMULTANEOUS (Alg. 1 verbatim) or CBVH_DESCENT_LARGER
   int early_exit;        // collide: stop a pose's traversal at its first hit
+  int capped;            // distance: dist holds per-pose caps on entry (cbvh_query_opts.capped)
 };
 
 // item pose word: bits 0..29 pose id, bit 30 = descend a, bit 31 = descend b
@@ -1570,7 +1571,14 @@ __global__ void init_kernel(Params p, int reset_stats) {
   int stride = gridDim.x * blockDim.x;
   for (int k = i; k < p.N; k += stride) {
     if (MODE == 0) { p.count[k] = 0u; p.hit[k] = 0; }
-    else p.dist_bits[k] = 0x7f800000u;  // +inf
+    else if (!p.capped) p.dist_bits[k] = 0x7f800000u;  // +inf
+    else {
+      // caller-supplied caps: NaN -> +inf (no cap), negative -> 0; the float
+      // bits of non-negative values order like uint32 (atomicMin)
+      const uint32_t b = p.dist_bits[k];
+      if (b & 0x80000000u) p.dist_bits[k] = 0u;
+      else if (b > 0x7f800000u) p.dist_bits[k] = 0x7f800000u;
+    }
   }
   if (i == 0) {
     p.ctl->error = 0u;
@@ -1713,7 +1721,7 @@ static DevTree make_tree(const cbvh_bvh* T) {
 template <int MODE, bool STATS, int KX>
 static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                      uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream, int descent,
-                     int early_exit) {
+                     int early_exit, int capped) {
   g_launches = 0;
   if (!A || !B || !d_ws) return set_error(CBVH_EINVAL, "null argument");
   if (N < 0 || N > 0x3fffffffLL) return set_error(CBVH_EINVAL, "N out of range [0, 2^30)");
@@ -1757,6 +1765,7 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   uint32_t* cont1 = cont0 + (size_t)kContCap * nfields(KX);
   p.descent = descent;
   p.early_exit = (MODE == 0 && early_exit) ? 1 : 0;
+  p.capped = (MODE == 1 && capped) ? 1 : 0;
   p.nwarps = s.warps;
   int ib = (int)((N + 255) / 256);
   ib = ib < 1 ? 1 : (ib > 4096 ? 4096 : ib);
@@ -1787,15 +1796,15 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
 template <int MODE, bool STATS>
 static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                   uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream, int descent,
-                  int early_exit) {
+                  int early_exit, int capped) {
   g_launches = 0;
   if (!A || !B) return set_error(CBVH_EINVAL, "null argument");
   if (A->h.kdop != 6) return set_error(CBVH_EINVAL, "k-DOP blobs bound the static model B only; A must be an AABB blob");
   switch (extra_axes(B)) {
-    case 0: return launch_kx<MODE, STATS, 0>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit);
-    case 4: return launch_kx<MODE, STATS, 4>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit);
-    case 6: return launch_kx<MODE, STATS, 6>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit);
-    case 10: return launch_kx<MODE, STATS, 10>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit);
+    case 0: return launch_kx<MODE, STATS, 0>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped);
+    case 4: return launch_kx<MODE, STATS, 4>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped);
+    case 6: return launch_kx<MODE, STATS, 6>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped);
+    case 10: return launch_kx<MODE, STATS, 10>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped);
   }
   return set_error(CBVH_EINVAL, "bad k-DOP");
 }
@@ -1921,19 +1930,20 @@ size_t cbvh_workspace_bytes(const cbvh_bvh* A, const cbvh_bvh* B, int64_t N, int
 
 static int opts_descent(const cbvh_query_opts* o) { return o ? o->descent : CBVH_DESCENT_LARGER; }
 static int opts_early(const cbvh_query_opts* o) { return o ? o->early_exit : 0; }
+static int opts_capped(const cbvh_query_opts* o) { return o ? o->capped : 0; }
 static int opts_stats(const cbvh_query_opts* o) { return o ? o->stats : 0; }
 
 int collide_batch_ex(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                      uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream, const cbvh_query_opts* o) {
   if (opts_stats(o))
-    return launch<0, true>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o));
-  return launch<0, false>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o));
+    return launch<0, true>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o));
+  return launch<0, false>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o));
 }
 int distance_batch_ex(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, float* d_min_dist,
                       void* d_ws, size_t ws_bytes, void* stream, const cbvh_query_opts* o) {
   if (opts_stats(o))
-    return launch<1, true>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o));
-  return launch<1, false>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o));
+    return launch<1, true>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o));
+  return launch<1, false>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o));
 }
 int collide_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                   uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream) {
@@ -1941,7 +1951,7 @@ int collide_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
 }
 int collide_batch_stats(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                         uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream) {
-  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1, 0};
+  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1, 0, 0};
   return collide_batch_ex(A, B, d_poses, N, d_hit, d_pair_count, d_ws, ws_bytes, stream, &o);
 }
 int distance_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, float* d_min_dist,
@@ -1950,7 +1960,7 @@ int distance_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, i
 }
 int distance_batch_stats(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N,
                          float* d_min_dist, void* d_ws, size_t ws_bytes, void* stream) {
-  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1, 0};
+  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1, 0, 0};
   return distance_batch_ex(A, B, d_poses, N, d_min_dist, d_ws, ws_bytes, stream, &o);
 }
 

@@ -186,6 +186,34 @@ def test_config1_distance(M, cfg1):
     assert rep["near_contact"] > 20
 
 
+def test_config1_distance_caps(M, cfg1):
+    # capped queries (cbvh_query_opts.capped): result = min(distance, cap),
+    # exact below the cap; caps above the oracle's distance change nothing,
+    # caps below it come back unchanged; NaN = no cap, negative = 0
+    w, tA, tB, delta = cfg1[:4]
+    A, B = build(M, w.A, 2, 8), build(M, w.B, 2, 8)
+    P = w.poses[:256]
+    d64, _ = O.distance(tA, tB, P)
+    Pt = torch.from_numpy(np.ascontiguousarray(P)).cuda()
+    ws = M.Workspace(A, B, 1)
+    far = d64 > 0.05
+    above = np.where(far, d64 * 1.01 + 1e-3, np.inf).astype(np.float32)
+    g = M.distance_batch(A, B, Pt, workspace=ws, caps=torch.from_numpy(above).cuda()).cpu().numpy()
+    M.check(ws)
+    check_distance(g, d64, delta, "cfg1 caps above")
+    below = np.where(far, d64 * 0.5, np.float32(np.nan)).astype(np.float32)
+    below[:4] = -1.0
+    g = M.distance_batch(A, B, Pt, workspace=ws, caps=torch.from_numpy(below).cuda()).cpu().numpy()
+    M.check(ws)
+    cap_rows = far.copy()
+    cap_rows[:4] = False
+    assert np.array_equal(g[cap_rows], below[cap_rows])
+    assert np.all(g[:4] == 0.0)
+    nan_rows = ~far
+    nan_rows[:4] = False
+    check_distance(g[nan_rows], d64[nan_rows], delta, "cfg1 caps nan")
+
+
 def test_contact_preset_collide_and_distance(M):
     # the paper's "distance of zero" preset: every pose at or near
     # contact — the band and the fp64 distance re-evaluation are exercised hardest
