@@ -91,7 +91,7 @@ __device__ __noinline__ bool coplanar2(const F* N, const TriT<F>& V, const TriT<
 // from the projections p[] of its vertices and their plane distances d[]
 // (k = the vertex alone on its side).
 #ifndef CBVH_MOLLER_SELECT
-#define CBVH_MOLLER_SELECT 0
+#define CBVH_MOLLER_SELECT 1  // interval case analysis as selects (measured 0.5-1 % faster on configs 5 and 3)
 #endif
 template <class F>
 __device__ __forceinline__ bool interval(const F p[3], const F d[3], F* t0, F* t1) {
