@@ -329,11 +329,11 @@ __device__ __forceinline__ PoseF load_pose(const float* poses, int i) {
 
 // ---------------------------------------------------------------- BV test
 
-#ifndef CBVH_DIST_CAXIS
-#define CBVH_DIST_CAXIS 1
+#ifndef CBVH_DIST_BOXB
+#define CBVH_DIST_BOXB 5  // world-AABB gap + centre axis: 4 alone is 2-4 % faster at config 4 but 17 % slower on config 2 distance; 7 no tighter
 #endif
-#ifndef CBVH_DIST_LAXIS
-#define CBVH_DIST_LAXIS 1
+#ifndef CBVH_DIST_LEAFB
+#define CBVH_DIST_LEAFB 4  // centroid axis only: 1 | 2 | 4 prune the same, measured 12 % slower (config 4)
 #endif
 #ifndef CBVH_SAT_EDGES
 #define CBVH_SAT_EDGES 0
@@ -392,24 +392,28 @@ __device__ __forceinline__ float sat_gap(const PoseF& P, const float alo[3], con
   }
 #endif
   if (WANT_LB) {
-    // Euclidean gaps: b against the world AABB of a, and a against the
-    // A-frame AABB of b (both contain the posed boxes)
-    float g0 = fmaxf(gw[0], 0.f), g1 = fmaxf(gw[1], 0.f), g2 = fmaxf(gw[2], 0.f);
-    float e = sqrtf(fmaf(g0, g0, fmaf(g1, g1, g2 * g2)));
-    g0 = fmaxf(ga[0], 0.f); g1 = fmaxf(ga[1], 0.f); g2 = fmaxf(ga[2], 0.f);
-    const float ea = sqrtf(fmaf(g0, g0, fmaf(g1, g1, g2 * g2)));
-#if CBVH_DIST_CAXIS
-    // the axis through the two box centres, u = Tw / |Tw|: |Tw| less the
-    // radii of both boxes on u (A's from Ta = R^T Tw) — for boxes far apart
-    // relative to their size this is nearly the true distance
-    const float T2 = fmaf(Tw[0], Tw[0], fmaf(Tw[1], Tw[1], Tw[2] * Tw[2]));
-    const float rs = fmaf(ha[0], fabsf(Ta[0]), fmaf(ha[1], fabsf(Ta[1]), fmaf(ha[2], fabsf(Ta[2]),
-                     fmaf(hb[0], fabsf(Tw[0]), fmaf(hb[1], fabsf(Tw[1]), hb[2] * fabsf(Tw[2]))))));
-    const float ec = T2 > 0.f ? (T2 - rs) * rsqrtf(T2) : 0.f;
-    *lb = fmaxf(fmaxf(fmaxf(e, ea), ec), 0.f) - eps;
-#else
-    *lb = fmaxf(fmaxf(e, ea), 0.f) - eps;
-#endif
+    // lower bounds on the box distance, CBVH_DIST_BOXB bits: 1 the Euclidean
+    // gap of b against the world AABB of a, 2 of a against the A-frame AABB
+    // of b (both contain the posed boxes), 4 the axis through the two box
+    // centres, u = Tw / |Tw|: |Tw| less the radii of both boxes on u (A's
+    // from Ta = R^T Tw) — nearly the true distance for boxes far apart
+    // relative to their size
+    float l = 0.f;
+    if (CBVH_DIST_BOXB & 1) {
+      const float g0 = fmaxf(gw[0], 0.f), g1 = fmaxf(gw[1], 0.f), g2 = fmaxf(gw[2], 0.f);
+      l = sqrtf(fmaf(g0, g0, fmaf(g1, g1, g2 * g2)));
+    }
+    if (CBVH_DIST_BOXB & 2) {
+      const float g0 = fmaxf(ga[0], 0.f), g1 = fmaxf(ga[1], 0.f), g2 = fmaxf(ga[2], 0.f);
+      l = fmaxf(l, sqrtf(fmaf(g0, g0, fmaf(g1, g1, g2 * g2))));
+    }
+    if (CBVH_DIST_BOXB & 4) {
+      const float T2 = fmaf(Tw[0], Tw[0], fmaf(Tw[1], Tw[1], Tw[2] * Tw[2]));
+      const float rs = fmaf(ha[0], fabsf(Ta[0]), fmaf(ha[1], fabsf(Ta[1]), fmaf(ha[2], fabsf(Ta[2]),
+                       fmaf(hb[0], fabsf(Tw[0]), fmaf(hb[1], fabsf(Tw[1]), hb[2] * fabsf(Tw[2]))))));
+      l = fmaxf(l, T2 > 0.f ? (T2 - rs) * rsqrtf(T2) : 0.f);
+    }
+    *lb = fmaxf(l, 0.f) - eps;
   }
   return gmax - eps;
 }
@@ -651,18 +655,32 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
 template <int DIR>
 __device__ CBVH_FILTER_ATTR uint32_t box_near_leaf(const PoseF& P, const float lo[3], const float hi[3],
                                                const float* tris, uint32_t leaf, float eps, float best,
-                                               float* lbmin) {
-  const uint32_t first = leaf & 0x1FFFFFFFu, cnt = ((leaf >> 29) & 3u) + 1;
+                                               float* lbmin, uint32_t todo) {
+  // only the triangles in `todo`: one the parent box's bound already put at
+  // or beyond the pose's best stays there for the child box (child ⊆ parent,
+  // best only decreases)
+  const uint32_t first = leaf & 0x1FFFFFFFu;
+  todo &= (2u << ((leaf >> 29) & 3u)) - 1u;
   float c[3], h[3];
   #pragma unroll
   for (int k = 0; k < 3; ++k) { c[k] = 0.5f * (lo[k] + hi[k]); h[k] = 0.5f * (hi[k] - lo[k]); }
   uint32_t m = 0;
   float lbm = FLT_MAX;
-  TriRec next = load_rec(tris, first);
+  *lbmin = lbm;
+  if (todo == 0u) return 0u;
+  uint32_t qn = (uint32_t)__ffs(todo) - 1u;
+  todo &= todo - 1u;
+  TriRec next = load_rec(tris, first + qn);
   #pragma unroll 1
-  for (uint32_t q = 0; q < cnt; ++q) {
+  while (true) {
     const TriRec cur = next;
-    if (q + 1 < cnt) next = load_rec(tris, first + q + 1);
+    const uint32_t q = qn;
+    const bool more = todo != 0u;
+    if (more) {
+      qn = (uint32_t)__ffs(todo) - 1u;
+      todo &= todo - 1u;
+      next = load_rec(tris, first + qn);
+    }
     const Tri L = rec_tri(cur);
     float v[3][3];
     #pragma unroll
@@ -677,37 +695,45 @@ __device__ CBVH_FILTER_ATTR uint32_t box_near_leaf(const PoseF& P, const float l
           v[u][k] = fmaf(P.R[k][0], L.v[u][0], fmaf(P.R[k][1], L.v[u][1], fmaf(P.R[k][2], L.v[u][2], P.t[k]))) - c[k];
       }
     }
-    float g2 = 0.f;
-    #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const float tlo = fminf(v[0][k], fminf(v[1][k], v[2][k]));
-      const float thi = fmaxf(v[0][k], fmaxf(v[1][k], v[2][k]));
-      const float g = fmaxf(0.f, fmaxf(tlo - h[k], -h[k] - thi));
-      g2 = fmaf(g, g, g2);
+    // separating-axis gaps (each a lower bound on the box-triangle
+    // distance), CBVH_DIST_LEAFB bits: 1 the box axes (triangle AABB gap),
+    // 2 the triangle normal, 4 the box-centre-to-centroid axis
+    float lb = 0.f;
+    if (CBVH_DIST_LEAFB & 1) {
+      float g2 = 0.f;
+      #pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float tlo = fminf(v[0][k], fminf(v[1][k], v[2][k]));
+        const float thi = fmaxf(v[0][k], fmaxf(v[1][k], v[2][k]));
+        const float g = fmaxf(0.f, fmaxf(tlo - h[k], -h[k] - thi));
+        g2 = fmaf(g, g, g2);
+      }
+      lb = sqrtf(g2);
     }
-    float e1[3], e2[3], n[3];
-    vsub(v[1], v[0], e1);
-    vsub(v[2], v[0], e2);
-    vcross(e1, e2, n);
-    const float nn = vdot(n, n);
-    const float rad_n = fmaf(fabsf(n[0]), h[0], fmaf(fabsf(n[1]), h[1], fabsf(n[2]) * h[2]));
-    const float gn = nn > 0.f ? (fabsf(vdot(n, v[0])) - rad_n) * rsqrtf(nn) : 0.f;
-#if CBVH_DIST_LAXIS
-    // the axis from the box centre (the origin here) to the triangle's
-    // centroid: the triangle's nearest projection less the box radius
-    float ct[3];
-    #pragma unroll
-    for (int k = 0; k < 3; ++k) ct[k] = (v[0][k] + v[1][k] + v[2][k]) * (1.f / 3.f);
-    const float c2 = fmaf(ct[0], ct[0], fmaf(ct[1], ct[1], ct[2] * ct[2]));
-    const float pmin = fminf(vdot(ct, v[0]), fminf(vdot(ct, v[1]), vdot(ct, v[2])));
-    const float rb = fmaf(fabsf(ct[0]), h[0], fmaf(fabsf(ct[1]), h[1], fabsf(ct[2]) * h[2]));
-    const float gc = c2 > 0.f ? (pmin - rb) * rsqrtf(c2) : 0.f;
-    const float lb = fmaxf(fmaxf(sqrtf(g2), gn), gc) - 2.f * eps;
-#else
-    const float lb = fmaxf(sqrtf(g2), gn) - 2.f * eps;
-#endif
+    if (CBVH_DIST_LEAFB & 2) {
+      float e1[3], e2[3], n[3];
+      vsub(v[1], v[0], e1);
+      vsub(v[2], v[0], e2);
+      vcross(e1, e2, n);
+      const float nn = vdot(n, n);
+      const float rad_n = fmaf(fabsf(n[0]), h[0], fmaf(fabsf(n[1]), h[1], fabsf(n[2]) * h[2]));
+      lb = fmaxf(lb, nn > 0.f ? (fabsf(vdot(n, v[0])) - rad_n) * rsqrtf(nn) : 0.f);
+    }
+    if (CBVH_DIST_LEAFB & 4) {
+      // the axis from the box centre (the origin here) to the triangle's
+      // centroid: the triangle's nearest projection less the box radius
+      float ct[3];
+      #pragma unroll
+      for (int k = 0; k < 3; ++k) ct[k] = (v[0][k] + v[1][k] + v[2][k]) * (1.f / 3.f);
+      const float c2 = fmaf(ct[0], ct[0], fmaf(ct[1], ct[1], ct[2] * ct[2]));
+      const float pmin = fminf(vdot(ct, v[0]), fminf(vdot(ct, v[1]), vdot(ct, v[2])));
+      const float rb = fmaf(fabsf(ct[0]), h[0], fmaf(fabsf(ct[1]), h[1], fabsf(ct[2]) * h[2]));
+      lb = fmaxf(lb, c2 > 0.f ? (pmin - rb) * rsqrtf(c2) : 0.f);
+    }
+    lb -= 2.f * eps;
     if (lb < best) m |= 1u << q;
     lbm = fminf(lbm, lb);
+    if (!more) break;
   }
   *lbmin = lbm;
   return m;
@@ -812,8 +838,8 @@ __device__ __forceinline__ float tri_box_gap(const Tri& V, const Tri& U) {
 // apart it is within ~size^2 / distance of the true distance, where the AABB
 // gap is off by ~size x tilt).  Projections are taken relative to V's
 // centroid so the magnitudes stay small.
-#ifndef CBVH_DIST_AXIS
-#define CBVH_DIST_AXIS 1
+#ifndef CBVH_DIST_TRIB
+#define CBVH_DIST_TRIB 3
 #endif
 __device__ __forceinline__ float tri_axis_gap(const Tri& V, const Tri& U) {
   float cv[3], u[3];
@@ -1048,10 +1074,10 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
         const float tmax0 = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
         const float best = __uint_as_float(__ldcg(&p.dist_bits[my_pose]));
         const float slack = 2e-6f * (tmax0 + p.A.maxabs + p.B.maxabs);
-        keep = tri_box_gap(TA, TB) - slack < best;
-#if CBVH_DIST_AXIS
-        if (keep) keep = tri_axis_gap(TA, TB) - slack < best;
-#endif
+        // CBVH_DIST_TRIB bits: 1 the triangle AABB gap, 2 the centroid axis
+        keep = true;
+        if (CBVH_DIST_TRIB & 1) keep = tri_box_gap(TA, TB) - slack < best;
+        if ((CBVH_DIST_TRIB & 2) && keep) keep = tri_axis_gap(TA, TB) - slack < best;
         if (STATS && keep) ++*exact;
       }
     }
@@ -1256,7 +1282,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
               }
               #pragma unroll
               for (int q = 0; q < 2 * KX; ++q) c.st[(F_XB + q) * kStack + slot] = (uint32_t)p.X.root[q];
-              c.st[F_LB * kStack + slot] = MODE == 0 ? 0xFFu : 0u;  // collide: inherited leaf masks (all)
+              c.st[F_LB * kStack + slot] = 0xFFu;  // inherited leaf masks: all (distance: lower bound 0)
             }
           }
           if (root_leafpair) nleaf += k; else top += k;
@@ -1349,8 +1375,10 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     }
     #pragma unroll
     for (int q = 0; q < 2 * KX; ++q) BX[q] = (int32_t)c.st[(F_XB + q) * kStack + slot];
-    const uint32_t item_w = c.st[F_LB * kStack + slot];  // distance: lower bound; collide: leaf masks
-    const float item_lb = __uint_as_float(item_w);
+    // leaf masks in bits 0-7; distance: the lower bound's float bits above
+    // (rounded down to a multiple of 256 ulp)
+    const uint32_t item_w = c.st[F_LB * kStack + slot];
+    const float item_lb = __uint_as_float(item_w & ~0xFFu);
     __syncwarp();
     top -= m;
     if (STATS) { s_exp += m; s_iter += passes; }
@@ -1378,6 +1406,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       // triangles of a leaf side the parent's refinement kept (collide; a
       // descended side is a new node: all)
       uint32_t mskA = 15u, mskB = 15u;
+      // (collide only: for distance the inherited masks rarely exclude a
+      // triangle and measured 4 % slower on config 4)
       if (MODE == 0 && CBVH_MASK_PROP) {
         if (!a_int) mskA = item_w & 15u;
         if (!b_int) mskB = (item_w >> 4) & 15u;
@@ -1452,13 +1482,13 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
           // a tighter pair bound)
           if (surv && (ctb & kLeafBit)) {
             float l2;
-            mskB = box_near_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps, best, &l2);
+            mskB = box_near_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps, best, &l2, mskB);
             lb = fmaxf(lb, l2);
             surv = mskB != 0u;
           }
           if (surv && (cta & kLeafBit)) {
             float l2;
-            mskA = box_near_leaf<1>(P, blo, bhi, p.A.tris, cta, eps, best, &l2);
+            mskA = box_near_leaf<1>(P, blo, bhi, p.A.tris, cta, eps, best, &l2, mskA);
             lb = fmaxf(lb, l2);
             surv = mskA != 0u;
           }
@@ -1504,8 +1534,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
           }
           #pragma unroll
           for (int q = 0; q < 2 * KX; ++q) c.st[(F_XB + q) * kStack + s2] = (uint32_t)CX[q];
-          if (MODE == 1) c.st[F_LB * kStack + s2] = __float_as_uint(lb);
-          else c.st[F_LB * kStack + s2] = (mskA & 15u) | ((mskB & 15u) << 4);
+          c.st[F_LB * kStack + s2] = (MODE == 1 ? (__float_as_uint(fmaxf(lb, 0.f)) & ~0xFFu) : 0u) |
+                                     (mskA & 15u) | ((mskB & 15u) << 4);
         }
         top += __popc(pm);
       }
