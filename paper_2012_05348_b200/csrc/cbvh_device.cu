@@ -506,27 +506,53 @@ __device__ __forceinline__ bool tri_boxes_overlap(const Tri& V, const Tri& U) {
 #ifndef CBVH_FOLD_CENTRE
 #define CBVH_FOLD_CENTRE 1
 #endif
+// axes of the box-triangle filter: 1 the box axes, 2 the triangle normal —
+// for A's boxes against B's triangles (DIR 0) and B's boxes against A's (DIR 1)
+#ifndef CBVH_COL_LEAFB0
+#define CBVH_COL_LEAFB0 3
+#endif
+#ifndef CBVH_COL_LEAFB1
+#define CBVH_COL_LEAFB1 1  // box axes only: B's boxes against A's small triangles (measured 2-5 % faster than 3 on configs 5, 3, 2)
+#endif
+// bit 4: the normal axis only when the triangle's extent exceeds this many box half extents
+#ifndef CBVH_NORMAL_RATIO
+#define CBVH_NORMAL_RATIO 2.0f
+#endif
+// evaluate every axis before deciding (no early return after the box axes)
+#ifndef CBVH_TRIBOX_NOBRANCH
+#define CBVH_TRIBOX_NOBRANCH 0
+#endif
+template <int AXES>
 __device__ __forceinline__ bool box_tri_overlap(const float c[3], const float h[3], const Tri& T, float eps) {
   float v[3][3];
   #pragma unroll
   for (int q = 0; q < 3; ++q)
     #pragma unroll
     for (int k = 0; k < 3; ++k) v[q][k] = CBVH_FOLD_CENTRE ? T.v[q][k] : T.v[q][k] - c[k];  // box-centred
-  #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const float tlo = fminf(v[0][k], fminf(v[1][k], v[2][k]));
-    const float thi = fmaxf(v[0][k], fmaxf(v[1][k], v[2][k]));
-    if (tlo > h[k] + eps || thi < -h[k] - eps) return false;
+  bool sep = false;
+  float text = 0.f, hmax = 0.f;  // the triangle's extent and the box's half extent (adaptive normal test)
+  if (AXES & 1) {
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float tlo = fminf(v[0][k], fminf(v[1][k], v[2][k]));
+      const float thi = fmaxf(v[0][k], fmaxf(v[1][k], v[2][k]));
+      sep = sep || tlo > h[k] + eps || thi < -h[k] - eps;
+      if (AXES & 4) { text = fmaxf(text, thi - tlo); hmax = fmaxf(hmax, h[k]); }
+    }
+    if (!CBVH_TRIBOX_NOBRANCH && sep) return false;
   }
   float e[3][3];
   vsub(v[1], v[0], e[0]);
   vsub(v[2], v[1], e[1]);
   vsub(v[0], v[2], e[2]);
-  float n[3];
-  vcross(e[0], e[1], n);
-  const float nrm = fabsf(n[0]) + fabsf(n[1]) + fabsf(n[2]);
-  const float rad_n = fmaf(fabsf(n[0]), h[0], fmaf(fabsf(n[1]), h[1], fabsf(n[2]) * h[2]));
-  if (fabsf(vdot(n, v[0])) > fmaf(eps, nrm, rad_n)) return false;
+  if ((AXES & 2) || ((AXES & 4) && text > CBVH_NORMAL_RATIO * hmax)) {
+    float n[3];
+    vcross(e[0], e[1], n);
+    const float nrm = fabsf(n[0]) + fabsf(n[1]) + fabsf(n[2]);
+    const float rad_n = fmaf(fabsf(n[0]), h[0], fmaf(fabsf(n[1]), h[1], fabsf(n[2]) * h[2]));
+    sep = sep || fabsf(vdot(n, v[0])) > fmaf(eps, nrm, rad_n);
+  }
+  if (sep) return false;
 #if CBVH_TRIBOX_EDGES
   #pragma unroll
   for (int i = 0; i < 3; ++i) {
@@ -632,7 +658,7 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
           W.v[v][k] = fmaf(P.R[k][0], L.v[v][0], fmaf(P.R[k][1], L.v[v][1], fmaf(P.R[k][2], L.v[v][2], P.t[k])));
     }
 #endif
-    if (box_tri_overlap(c, h, W, eps)) m |= 1u << q;
+    if (box_tri_overlap<DIR == 0 ? CBVH_COL_LEAFB0 : CBVH_COL_LEAFB1>(c, h, W, eps)) m |= 1u << q;
     if (!more) break;
   }
   return m;
