@@ -949,6 +949,104 @@ __device__ __forceinline__ int small_div(int k, int d) {
 // all triangles of a leaf: low (ntri) bits set
 __device__ __forceinline__ uint32_t full_mask(uint32_t t) { return (2u << ((t >> 29) & 3u)) - 1u; }
 
+// The distance of triangle pair (ia, ib) under pose P as the leaf phase
+// reports it: fp32 in A's frame; fp32 error here is ~1e-7 x (|t| + model
+// extents), so candidates too small for a 1e-5 relative bound are
+// re-evaluated in fp64.
+__device__ __forceinline__ float pair_distance(const Params& p, const PoseF& P, const Tri& TA, const Tri& TB,
+                                               uint32_t ia, uint32_t ib) {
+  float d = tri_tri_dist(TA, TB);
+  const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
+  if (d < 0.05f * (tmax + p.A.maxabs + p.B.maxabs)) d = tri_dist_fp64(P, p.A.tris, ia, p.B.tris, ib);
+  return d;
+}
+
+// Greedy dive (distance): one pose per thread descends from the root pair,
+// always into the child pair with the smallest lower bound (the larger-first
+// side, or the non-leaf side), to one leaf pair, and records the smallest
+// distance among its triangle pairs as the pose's starting best.  That is the
+// distance of real triangle pairs computed exactly as the leaf phase computes
+// it, so the traversal's result is unchanged (min over a superset); it only
+// prunes from the start instead of from +inf (reading R26).
+template <int KX>
+__global__ void __launch_bounds__(128) dive_kernel(const __grid_constant__ Params p) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.N) return;
+  const PoseF P = load_pose(p.poses, i);
+  const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
+  const float eps = 2e-6f * (tmax + p.A.maxabs + p.B.maxabs);
+  uint32_t ta = p.A.root_topo, tb = p.B.root_topo;
+  int32_t BA[6], BB[6], BX[2 * KX + 1];
+  #pragma unroll
+  for (int q = 0; q < 6; ++q) { BA[q] = p.A.root[q]; BB[q] = p.B.root[q]; }
+  #pragma unroll
+  for (int q = 0; q < 2 * KX; ++q) BX[q] = p.X.root[q];
+  #pragma unroll 1
+  for (int guard = 0; guard < 128; ++guard) {
+    const bool la = (ta & kLeafBit) != 0, lb = (tb & kLeafBit) != 0;
+    if (la && lb) break;
+    const bool descA = !la && (lb || (descent_flags(CBVH_DESCENT_LARGER, ta, tb, BA, BB, p.A, p.B) & kDescA));
+    const uint32_t t = descA ? ta : tb;
+    const uint32_t first = t & 0x0FFFFFFFu, nc = ((t >> 28) & 7u) + 1;
+    float best = FLT_MAX;
+    uint32_t bt = 0;
+    int32_t bbox[6], bx[2 * KX + 1];
+    #pragma unroll 1
+    for (uint32_t k = 0; k < nc; ++k) {
+      int32_t C[6], CX[2 * KX + 1];
+      uint32_t ct;
+      float alo[3], ahi[3], blo[3], bhi[3], l;
+      if (descA) {
+        ct = __ldg(p.A.topo + first + k);
+        fetch_child_box(p.A, first + k, BA, C);
+        words_to_float(p.A, C, alo, ahi);
+        words_to_float(p.B, BB, blo, bhi);
+      } else {
+        ct = __ldg(p.B.topo + first + k);
+        if constexpr (KX > 0) fetch_child_kdop<KX>(p.B, first + k, BB, BX, C, CX);
+        else fetch_child_box(p.B, first + k, BB, C);
+        words_to_float(p.A, BA, alo, ahi);
+        words_to_float(p.B, C, blo, bhi);
+      }
+      sat_gap<true>(P, alo, ahi, blo, bhi, eps, &l);
+      if (k == 0 || l < best) {
+        best = l;
+        bt = ct;
+        #pragma unroll
+        for (int q = 0; q < 6; ++q) bbox[q] = C[q];
+        if constexpr (KX > 0) {
+          #pragma unroll
+          for (int q = 0; q < 2 * KX; ++q) bx[q] = CX[q];
+        }
+      }
+    }
+    if (descA) {
+      ta = bt;
+      #pragma unroll
+      for (int q = 0; q < 6; ++q) BA[q] = bbox[q];
+    } else {
+      tb = bt;
+      #pragma unroll
+      for (int q = 0; q < 6; ++q) BB[q] = bbox[q];
+      if constexpr (KX > 0) {
+        #pragma unroll
+        for (int q = 0; q < 2 * KX; ++q) BX[q] = bx[q];
+      }
+    }
+  }
+  if (!((ta & kLeafBit) && (tb & kLeafBit))) return;
+  const uint32_t fa = ta & 0x1FFFFFFFu, na = ((ta >> 29) & 3u) + 1;
+  const uint32_t fb = tb & 0x1FFFFFFFu, nb = ((tb >> 29) & 3u) + 1;
+  float d = FLT_MAX;
+  #pragma unroll 1
+  for (uint32_t u = 0; u < nb; ++u) {
+    const Tri TB = to_local(P, load_tri(p.B.tris, fb + u));
+    #pragma unroll 1
+    for (uint32_t v = 0; v < na; ++v) d = fminf(d, pair_distance(p, P, load_tri(p.A.tris, fa + v), TB, fa + v, fb + u));
+  }
+  atomicMin(&p.dist_bits[i], __float_as_uint(d));
+}
+
 // per-warp constant context (registers); mutable counters live in the kernel
 struct WarpCtx {
   uint32_t* st;     // stack SoA [nfields(KX)][kStack]
@@ -984,12 +1082,7 @@ __device__ __forceinline__ void exact_batch(const Params& p, const WarpCtx c, in
     if (MODE == 0) {
       hit = tri_tri_overlap(TA, TB);
     } else {
-      d = tri_tri_dist(TA, TB);
-      // fp32 error here is ~1e-7 x (|t| + model extents); candidates whose
-      // distance is too small for a 1e-5 relative bound are re-evaluated in
-      // fp64
-      const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
-      if (d < 0.05f * (tmax + p.A.maxabs + p.B.maxabs)) d = tri_dist_fp64(P, p.A.tris, ia, p.B.tris, ib);
+      d = pair_distance(p, P, TA, TB, ia, ib);
     }
   }
   if (MODE == 0) {
@@ -1735,6 +1828,17 @@ static size_t workspace_for_warps(int warps, int kx) {
 // extra k-DOP axes of B (0 for an AABB blob)
 static int extra_axes(const cbvh_bvh* B) { return B ? (int)B->h.kdop / 2 - 3 : 0; }
 
+// Greedy dive before a distance traversal (reading R26); CBVH_DIVE=0 turns it
+// off (A/B only).
+static bool dive_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* env = std::getenv("CBVH_DIVE");
+    on = (env && *env) ? (std::atoi(env) != 0) : 1;
+  }
+  return on != 0;
+}
+
 // Phase schedule: budgets of the bounded phases, then one
 // unbounded phase.  CBVH_PHASES="b0,b1,..." overrides (tuning only).
 static int phase_budgets(int* out) {
@@ -1833,6 +1937,12 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "init_kernel launch");
   if (N == 0) return CBVH_OK;
+  if (MODE == 1 && dive_enabled()) {
+    dive_kernel<KX><<<(int)((N + 127) / 128), 128, 0, st>>>(p);
+    g_launches++;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "dive_kernel launch");
+  }
   int budgets[kMaxPhases];
   const int nb = phase_budgets(budgets);
   if (g_ev_start) cudaEventRecord(g_ev_start, st);
