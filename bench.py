@@ -294,14 +294,25 @@ def run(args):
     alg_bytes = st["record_bytes"] + st["tri_bytes"] + N * (48 + 5)
     peaks = measured_peaks()
     achieved = alg_bytes / kern_s / 1e9
-    traffic = None
+    traffic, nc = None, {}
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(f"cfg{args.config}", {}).get("dram_bytes_per_launch")
+                nc = json.load(f).get(f"cfg{args.config}", {})
+            traffic = nc.get("dram_bytes_per_launch")
         except (OSError, ValueError):
-            traffic = None
+            traffic, nc = None, {}
+    # the issue ceiling the kernel actually runs into: warp
+    # instructions of the committed ncu capture over the live kernel time,
+    # against 148 SMs x 4 schedulers x the max SM clock
+    issue = None
+    winst = nc.get("warp_inst_per_launch") if not distance and args.layout == "delta" and args.kdop == 6 else None
+    if winst:
+        ipeak = 148 * 4 * peaks.get("sm_max_mhz", 1965.0) * 1e6
+        issue = {"bound": "issue", "achieved": winst / kern_s, "peak": ipeak, "unit": "warp inst/s",
+                 "frac": winst / kern_s / ipeak, "simt_efficiency": nc.get("thread_inst_per_warp_inst", 0) / 32,
+                 "source": "warp instructions of all phases from profiles/ncu_traffic.json (ncu), live kernel time"}
 
     # ---- end-to-end through the public API with host buffers (pinned)
     hit_h = torch.empty(N, dtype=torch.uint8, pin_memory=True)
@@ -348,6 +359,7 @@ def run(args):
                          "kernel_ms": 1e3 * kern_s,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "peak_source": peaks["_source"] + " hbm_gbs (copy bandwidth)"},
+            "roofline_issue": issue,
             "stats": st,
             "e2e": {"value": aggregate_rate(N, args.steps, world, E), "unit": UNIT,
                     "h2d_bytes_per_step": int(poses_h.numel() * 4),
