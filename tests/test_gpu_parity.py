@@ -459,6 +459,45 @@ def test_load_balancing_phases_do_not_change_results(M, tmp_path, phases):
         assert int(res["variant"]["dumped"]) > 0  # the schedule really moved work between launches
 
 
+_DIVE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2012_05348_b200 as M
+from workloads import generators as G
+out = {{}}
+for cfg, n, preset in ((4, 8192, "random"), (3, 8192, "contact"), (2, 4096, "random")):
+    w = G.make_config(cfg, num_poses=n, preset=preset)
+    A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet).to_device()
+    B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet).to_device()
+    P = torch.from_numpy(w.poses).cuda()
+    wd = M.Workspace(A, B, 1)
+    d = M.distance_batch(A, B, P, workspace=wd)
+    M.check(wd)
+    out["d%d" % cfg] = d.cpu().numpy()
+np.savez({out!r}, **out)
+"""
+
+
+def test_greedy_dive_does_not_change_distances(M, tmp_path):
+    # the dive (reading R26) only seeds each pose's best with a real pair
+    # distance computed as the leaf phase computes it: with and without it the
+    # distances are bit-identical (configs 4, 3 contact, 2)
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for tag in ("0", "1"):
+        out = str(tmp_path / f"dive{tag}.npz")
+        e = dict(os.environ)
+        e["CBVH_DIVE"] = tag
+        subprocess.run([sys.executable, "-c", _DIVE_SCRIPT.format(root=root, out=out)], env=e, check=True,
+                       timeout=600)
+        res[tag] = np.load(out)
+    for k in ("d4", "d3", "d2"):
+        assert np.array_equal(res["0"][k], res["1"][k]), k
+
+
 def test_config5_4x_poses_sampled(M):
     # 4,194,304 poses in one call (4x the headline batch): hit == (count > 0)
     # everywhere, the first 1M poses equal the 1M-pose call, and a sample of
