@@ -967,80 +967,24 @@ __device__ __forceinline__ float pair_distance(const Params& p, const PoseF& P, 
   return d;
 }
 
-// Greedy dive (distance): one pose per thread descends from the root pair,
-// always into the child pair with the smallest lower bound (the larger-first
-// side, or the non-leaf side), to one leaf pair, and records the smallest
-// distance among its triangle pairs as the pose's starting best.  That is the
-// distance of real triangle pairs computed exactly as the leaf phase computes
-// it, so the traversal's result is unchanged (min over a superset); it only
-// prunes from the start instead of from +inf (reading R26).
+// Greedy dive (distance): one pose per thread runs a beam search of width W
+// from the root pair — each step expands every beam entry (the larger-first
+// side, or the non-leaf side), scores the children by the box lower bound and
+// keeps the W best; a kept leaf pair is evaluated (its triangle pairs'
+// distances, computed exactly as the leaf phase computes them) and leaves the
+// beam.  The smallest distance found becomes the pose's starting best.  These
+// are distances of real triangle pairs, so the traversal's result is unchanged
+// (min over a superset of the same values); it only prunes from the start
+// instead of from +inf (reading R26).
 template <int KX>
-__global__ void __launch_bounds__(128) dive_kernel(const __grid_constant__ Params p) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p.N) return;
-  const PoseF P = load_pose(p.poses, i);
-  const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
-  const float eps = 2e-6f * (tmax + p.A.maxabs + p.B.maxabs);
-  uint32_t ta = p.A.root_topo, tb = p.B.root_topo;
+struct DiveEntry {
+  uint32_t ta, tb;
+  float lb;
   int32_t BA[6], BB[6], BX[2 * KX + 1];
-  #pragma unroll
-  for (int q = 0; q < 6; ++q) { BA[q] = p.A.root[q]; BB[q] = p.B.root[q]; }
-  #pragma unroll
-  for (int q = 0; q < 2 * KX; ++q) BX[q] = p.X.root[q];
-  #pragma unroll 1
-  for (int guard = 0; guard < 128; ++guard) {
-    const bool la = (ta & kLeafBit) != 0, lb = (tb & kLeafBit) != 0;
-    if (la && lb) break;
-    const bool descA = !la && (lb || (descent_flags(CBVH_DESCENT_LARGER, ta, tb, BA, BB, p.A, p.B) & kDescA));
-    const uint32_t t = descA ? ta : tb;
-    const uint32_t first = t & 0x0FFFFFFFu, nc = ((t >> 28) & 7u) + 1;
-    float best = FLT_MAX;
-    uint32_t bt = 0;
-    int32_t bbox[6], bx[2 * KX + 1];
-    #pragma unroll 1
-    for (uint32_t k = 0; k < nc; ++k) {
-      int32_t C[6], CX[2 * KX + 1];
-      uint32_t ct;
-      float alo[3], ahi[3], blo[3], bhi[3], l;
-      if (descA) {
-        ct = __ldg(p.A.topo + first + k);
-        fetch_child_box(p.A, first + k, BA, C);
-        words_to_float(p.A, C, alo, ahi);
-        words_to_float(p.B, BB, blo, bhi);
-      } else {
-        ct = __ldg(p.B.topo + first + k);
-        if constexpr (KX > 0) fetch_child_kdop<KX>(p.B, first + k, BB, BX, C, CX);
-        else fetch_child_box(p.B, first + k, BB, C);
-        words_to_float(p.A, BA, alo, ahi);
-        words_to_float(p.B, C, blo, bhi);
-      }
-      sat_gap<true>(P, alo, ahi, blo, bhi, eps, &l);
-      if (k == 0 || l < best) {
-        best = l;
-        bt = ct;
-        #pragma unroll
-        for (int q = 0; q < 6; ++q) bbox[q] = C[q];
-        if constexpr (KX > 0) {
-          #pragma unroll
-          for (int q = 0; q < 2 * KX; ++q) bx[q] = CX[q];
-        }
-      }
-    }
-    if (descA) {
-      ta = bt;
-      #pragma unroll
-      for (int q = 0; q < 6; ++q) BA[q] = bbox[q];
-    } else {
-      tb = bt;
-      #pragma unroll
-      for (int q = 0; q < 6; ++q) BB[q] = bbox[q];
-      if constexpr (KX > 0) {
-        #pragma unroll
-        for (int q = 0; q < 2 * KX; ++q) BX[q] = bx[q];
-      }
-    }
-  }
-  if (!((ta & kLeafBit) && (tb & kLeafBit))) return;
+};
+
+template <int KX>
+__device__ __forceinline__ float dive_leaf_pair(const Params& p, const PoseF& P, uint32_t ta, uint32_t tb) {
   const uint32_t fa = ta & 0x1FFFFFFFu, na = ((ta >> 29) & 3u) + 1;
   const uint32_t fb = tb & 0x1FFFFFFFu, nb = ((tb >> 29) & 3u) + 1;
   float d = FLT_MAX;
@@ -1050,7 +994,83 @@ __global__ void __launch_bounds__(128) dive_kernel(const __grid_constant__ Param
     #pragma unroll 1
     for (uint32_t v = 0; v < na; ++v) d = fminf(d, pair_distance(p, P, load_tri(p.A.tris, fa + v), TB, fa + v, fb + u));
   }
-  atomicMin(&p.dist_bits[i], __float_as_uint(d));
+  return d;
+}
+
+constexpr int64_t kDiveWideMinN = 16384;
+#ifndef CBVH_DIVE_BEAM
+#define CBVH_DIVE_BEAM 8  // measured 1 / 2 / 4 / 8 / 16 / 32: 8 best on configs 4, 3, 3 contact, 2
+#endif
+template <int KX, int W>
+__global__ void __launch_bounds__(128) dive_kernel(const __grid_constant__ Params p) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.N) return;
+  const PoseF P = load_pose(p.poses, i);
+  const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
+  const float eps = 2e-6f * (tmax + p.A.maxabs + p.B.maxabs);
+  DiveEntry<KX> beam[W], cand[W];
+  int nb = 1, nc;
+  beam[0].ta = p.A.root_topo;
+  beam[0].tb = p.B.root_topo;
+  beam[0].lb = 0.f;
+  #pragma unroll
+  for (int q = 0; q < 6; ++q) { beam[0].BA[q] = p.A.root[q]; beam[0].BB[q] = p.B.root[q]; }
+  #pragma unroll
+  for (int q = 0; q < 2 * KX; ++q) beam[0].BX[q] = p.X.root[q];
+  float dmin = __uint_as_float(__ldcg(&p.dist_bits[i]));  // +inf, or the caller's cap
+  if ((beam[0].ta & kLeafBit) && (beam[0].tb & kLeafBit)) {
+    dmin = fminf(dmin, dive_leaf_pair<KX>(p, P, beam[0].ta, beam[0].tb));
+    nb = 0;
+  }
+  #pragma unroll 1
+  for (int step = 0; step < 128 && nb > 0; ++step) {
+    nc = 0;
+    #pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+      const DiveEntry<KX>& E = beam[b];
+      const bool la = (E.ta & kLeafBit) != 0, lb = (E.tb & kLeafBit) != 0;
+      const bool descA = !la && (lb || (descent_flags(CBVH_DESCENT_LARGER, E.ta, E.tb, E.BA, E.BB, p.A, p.B) & kDescA));
+      const uint32_t t = descA ? E.ta : E.tb;
+      const uint32_t first = t & 0x0FFFFFFFu, n = ((t >> 28) & 7u) + 1;
+      #pragma unroll 1
+      for (uint32_t k = 0; k < n; ++k) {
+        DiveEntry<KX> C = E;
+        float alo[3], ahi[3], blo[3], bhi[3], l;
+        if (descA) {
+          C.ta = __ldg(p.A.topo + first + k);
+          fetch_child_box(p.A, first + k, E.BA, C.BA);
+        } else {
+          C.tb = __ldg(p.B.topo + first + k);
+          if constexpr (KX > 0) fetch_child_kdop<KX>(p.B, first + k, E.BB, E.BX, C.BB, C.BX);
+          else fetch_child_box(p.B, first + k, E.BB, C.BB);
+        }
+        words_to_float(p.A, C.BA, alo, ahi);
+        words_to_float(p.B, C.BB, blo, bhi);
+        sat_gap<true>(P, alo, ahi, blo, bhi, eps, &l);
+        if (l >= dmin) continue;
+        C.lb = l;
+        // keep the W smallest bounds (insertion into the sorted candidates)
+        int pos = nc < W ? nc : W;
+        while (pos > 0 && cand[pos - 1].lb > l) {
+          if (pos < W) cand[pos] = cand[pos - 1];
+          --pos;
+        }
+        if (pos < W) {
+          cand[pos] = C;
+          if (nc < W) ++nc;
+        }
+      }
+    }
+    // kept leaf pairs are evaluated and leave the beam
+    nb = 0;
+    #pragma unroll 1
+    for (int c = 0; c < nc; ++c) {
+      if (cand[c].lb >= dmin) continue;
+      if ((cand[c].ta & kLeafBit) && (cand[c].tb & kLeafBit)) dmin = fminf(dmin, dive_leaf_pair<KX>(p, P, cand[c].ta, cand[c].tb));
+      else beam[nb++] = cand[c];
+    }
+  }
+  atomicMin(&p.dist_bits[i], __float_as_uint(dmin));
 }
 
 // per-warp constant context (registers); mutable counters live in the kernel
@@ -1954,7 +1974,11 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   if (e != cudaSuccess) return cuda_fail(e, "init_kernel launch");
   if (N == 0) return CBVH_OK;
   if (MODE == 1 && dive_enabled()) {
-    dive_kernel<KX><<<(int)((N + 127) / 128), 128, 0, st>>>(p);
+    // one thread per pose runs the beam serially: for a batch that does not
+    // fill the GPU (< 16k poses) that latency is not hidden, so a width-1
+    // dive is used there (config 1 contact: 0.99 ms vs 1.98 ms at width 8)
+    if (N >= kDiveWideMinN) dive_kernel<KX, CBVH_DIVE_BEAM><<<(int)((N + 127) / 128), 128, 0, st>>>(p);
+    else dive_kernel<KX, 1><<<(int)((N + 127) / 128), 128, 0, st>>>(p);
     g_launches++;
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "dive_kernel launch");
