@@ -156,7 +156,12 @@ int collide_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
 
 /* distance_batch — separation-distance variant:
  * d_min_dist[i] = min over triangle pairs of the Euclidean distance under
- * pose i (0 when any pair intersects), fp32.  Arguments as collide_batch. */
+ * pose i (0 when any pair intersects), fp32.  Arguments as collide_batch.
+ * Launches init, one dive kernel (a beam search that seeds each pose's best
+ * with a real triangle-pair distance; R26) and the traversal
+ * phases, all on `stream`.  Accuracy: within 1e-5 relative of the fp64
+ * distance of the fp32 inputs (candidates below 0.05 x (|t| + extents) are
+ * re-evaluated in fp64). */
 int distance_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N,
                    float* d_min_dist, void* d_ws, size_t ws_bytes, void* stream);
 

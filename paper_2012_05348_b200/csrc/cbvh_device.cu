@@ -17,9 +17,11 @@
 //     rounding (lo down, hi up) so the decoded box always contains the node.
 //   * checkPrimitives: Möller's interval test, fp32, in A's local
 //     frame (B's triangle is mapped by R^T (v - t)), closed triangles.
-//   * distance variant: box lower bounds prune against
-//     the pose's best distance; leaves use the exact triangle–triangle
-//     distance (0 if they intersect).
+//   * distance variant: separating-axis lower bounds
+//     (box gaps and the axis through the centres, reading R24) prune against
+//     the pose's best distance, which a beam-search dive seeds with a real
+//     leaf-pair distance before the traversal (R26); leaves use the exact
+//     triangle–triangle distance (0 if they intersect).
 //
 // Execution model: a persistent grid; each warp owns a
 // node-pair stack in shared memory (SoA, spilled to a per-warp global area
