@@ -362,6 +362,44 @@ def test_config4_distance_full_size_sampled(M):
     print("cfg4", rep)
 
 
+def test_config3_contact_distance_full_size_sampled(M):
+    # the paper's zero-distance preset at config 3's full size (262,144
+    # poses, the width-8 dive active): sampled poses against the fp64 oracle
+    w = G.make_config(3, preset="contact")
+    A, B = build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet)
+    d = run_distance(M, A, B, w.poses)
+    assert np.all(np.isfinite(d)) and np.all(d >= 0)
+    idx = _sample(len(w.poses), 48, 31)
+    tA, tB = oracle_trees(w)
+    d64, _ = O.distance(tA, tB, w.poses[idx])
+    rep = check_distance(d[idx], d64, O.band_delta(w.A.vertices), "cfg3 contact")
+    print("cfg3 contact distance", rep)
+
+
+def test_config4_capped_full_size_sampled(M):
+    # caps at config 4's full size: result = min(distance, cap) on every pose
+    # (cap 3.5 falls inside the distance range [2.42, ~5]); sampled against
+    # the oracle, and exactly the uncapped result wherever that is below 3.5
+    w = G.make_config(4)
+    A, B = build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet)
+    d = run_distance(M, A, B, w.poses)
+    P = torch.from_numpy(w.poses).cuda()
+    ws = M.Workspace(A, B, 1)
+    cap = np.float32(3.5)
+    dc = M.distance_batch(A, B, P, workspace=ws, caps=torch.full((len(P),), float(cap), device="cuda")).cpu().numpy()
+    M.check(ws)
+    below = d < cap
+    assert 0 < below.sum() < len(d)
+    assert np.array_equal(dc[below], d[below])
+    assert np.all(dc[~below] == cap)
+    idx = _sample(len(w.poses), 64, 41)
+    tA, tB = oracle_trees(w)
+    d64, _ = O.distance(tA, tB, w.poses[idx])
+    ref = np.minimum(d64, float(cap))
+    rel = np.abs(dc[idx] - ref) / ref
+    assert rel.max() <= 1e-5
+
+
 def test_config5_layouts_agree_full_size(M):
     # full config 5 batch: fp16 / fp32 layouts count exactly what delta counts
     w = G.make_config(5)
