@@ -516,19 +516,11 @@ __device__ __forceinline__ bool tri_boxes_overlap(const Tri& V, const Tri& U) {
 #ifndef CBVH_COL_LEAFB1
 #define CBVH_COL_LEAFB1 1  // box axes only: B's boxes against A's small triangles (measured 2-5 % faster than 3 on configs 5, 3, 2)
 #endif
-// bit 4: the normal axis only when the triangle's extent exceeds this many box half extents
 #ifndef CBVH_PAIR_AFILTER
 #define CBVH_PAIR_AFILTER 2
 #endif
 #ifndef CBVH_PAIR_RATIO
 #define CBVH_PAIR_RATIO 1.5f  // measured: config 5 -4.5 %, configs 3 / 2 +1 / +2 % (always: config 3 -3.5 %; never: config 5 +6 %)
-#endif
-#ifndef CBVH_NORMAL_RATIO
-#define CBVH_NORMAL_RATIO 2.0f
-#endif
-// evaluate every axis before deciding (no early return after the box axes)
-#ifndef CBVH_TRIBOX_NOBRANCH
-#define CBVH_TRIBOX_NOBRANCH 0
 #endif
 template <int AXES>
 __device__ __forceinline__ bool box_tri_overlap(const float c[3], const float h[3], const Tri& T, float eps) {
@@ -538,22 +530,20 @@ __device__ __forceinline__ bool box_tri_overlap(const float c[3], const float h[
     #pragma unroll
     for (int k = 0; k < 3; ++k) v[q][k] = CBVH_FOLD_CENTRE ? T.v[q][k] : T.v[q][k] - c[k];  // box-centred
   bool sep = false;
-  float text = 0.f, hmax = 0.f;  // the triangle's extent and the box's half extent (adaptive normal test)
   if (AXES & 1) {
     #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const float tlo = fminf(v[0][k], fminf(v[1][k], v[2][k]));
       const float thi = fmaxf(v[0][k], fmaxf(v[1][k], v[2][k]));
       sep = sep || tlo > h[k] + eps || thi < -h[k] - eps;
-      if (AXES & 4) { text = fmaxf(text, thi - tlo); hmax = fmaxf(hmax, h[k]); }
     }
-    if (!CBVH_TRIBOX_NOBRANCH && sep) return false;
+    if (sep) return false;
   }
   float e[3][3];
   vsub(v[1], v[0], e[0]);
   vsub(v[2], v[1], e[1]);
   vsub(v[0], v[2], e[2]);
-  if ((AXES & 2) || ((AXES & 4) && text > CBVH_NORMAL_RATIO * hmax)) {
+  if (AXES & 2) {
     float n[3];
     vcross(e[0], e[1], n);
     const float nrm = fabsf(n[0]) + fabsf(n[1]) + fabsf(n[2]);
