@@ -39,6 +39,33 @@ def test_library_exports_every_header_symbol():
     assert set(L.EXPORTS) == names
 
 
+def test_ctypes_structs_match_header(tmp_path):
+    # the binding's ctypes mirrors of the ABI structs must have the C layout:
+    # compile a probe against include/cbvh.h that prints sizeof and every
+    # field offset, and compare with ctypes
+    import ctypes
+    import subprocess
+    structs = [L.cbvh_mesh, L.cbvh_build_opts, L.cbvh_header, L.cbvh_info, L.cbvh_bvh, L.cbvh_stats,
+               L.cbvh_query_opts]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "cbvh.h"', "int main(void) {"]
+    for S in structs:
+        lines.append(f'  printf("{S.__name__} %zu\\n", sizeof({S.__name__}));')
+        for f, _ in S._fields_:
+            lines.append(f'  printf("{S.__name__}.{f} %zu\\n", offsetof({S.__name__}, {f}));')
+    lines.append("  return 0;\n}")
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    inc = L.HERE + "/../include"
+    subprocess.run(["gcc", "-std=c11", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], check=True, capture_output=True,
+                                                 text=True).stdout.splitlines())
+    for S in structs:
+        assert int(got[S.__name__]) == ctypes.sizeof(S), S.__name__
+        for f, _ in S._fields_:
+            assert int(got[f"{S.__name__}.{f}"]) == getattr(S, f).offset, f"{S.__name__}.{f}"
+
+
 @pytest.mark.parametrize("B", [2, 4, 8])
 @pytest.mark.parametrize("bits", [2, 4, 5, 8, 11, 16])
 def test_invariants_config1(cfg1, B, bits):
