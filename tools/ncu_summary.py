@@ -28,6 +28,9 @@ KEYS = [
     "lts__t_sectors_srcunit_tex_op_read.sum",
     "dram__bytes_read.sum",
     "dram__bytes_write.sum",
+    "dram__bytes.sum.per_second",
+    "lts__t_sectors.sum",
+    "lts__t_sectors.sum.per_second",
 ]
 
 
