@@ -400,6 +400,37 @@ def test_config4_capped_full_size_sampled(M):
     assert rel.max() <= 1e-5
 
 
+@pytest.mark.parametrize("layout,kdop", [("fp16", 6), ("fp32", 6), ("delta", 14)])
+def test_config4_distance_layouts_sampled(M, layout, kdop):
+    # the absolute layouts (the paper's half / float comparison) and a k-DOP
+    # environment through the distance kernel at config 4's full size: the
+    # same distances as the delta-AABB blobs wherever both are exact, and the
+    # oracle's on a sample
+    w = G.make_config(4)
+    A = build(M, w.A, w.branching, w.bits, w.treelet, layout=layout)
+    B = build(M, w.B, w.branching, w.bits, w.treelet, layout=layout, kdop=kdop)
+    d = run_distance(M, A, B, w.poses)
+    ref = run_distance(M, build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet),
+                       w.poses)
+    assert np.max(np.abs(d - ref) / ref) <= 2e-5
+    idx = _sample(len(w.poses), 32, 51)
+    tA, tB = oracle_trees(w)
+    d64, _ = O.distance(tA, tB, w.poses[idx])
+    check_distance(d[idx], d64, O.band_delta(w.A.vertices), f"cfg4 {layout} k={kdop}")
+
+
+def test_config3_contact_early_exit_full_size(M):
+    # zero-distance preset at full size: early-exit hit flags equal the
+    # exhaustive ones on all 262,144 poses; counts are lower bounds >= 1 on hits
+    w = G.make_config(3, preset="contact")
+    A, B = build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet)
+    h1, c1 = run_collide(M, A, B, w.poses)
+    h2, c2 = run_collide(M, A, B, w.poses, early_exit=True)
+    assert np.array_equal(h1, h2)
+    assert np.array_equal(c2 > 0, h2 == 1) and np.all(c2 <= c1)
+    assert h1.sum() > len(h1) // 4
+
+
 def test_config5_layouts_agree_full_size(M):
     # full config 5 batch: fp16 / fp32 layouts count exactly what delta counts
     w = G.make_config(5)
