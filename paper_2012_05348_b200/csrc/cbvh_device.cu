@@ -915,10 +915,14 @@ __device__ __noinline__ float tri_dist_fp64(const PoseF& P, const float* trisA, 
 // the traversal kernel
 // ----------------------------------------------------------------------------
 
+#ifndef CBVH_SMEM_BOXES
+#define CBVH_SMEM_BOXES 2  // bit 0: collide, bit 1: distance (measured: distance config 4 -6 %, collide +1.5..2 %)
+#endif
+__host__ __device__ constexpr bool smem_boxes(int mode) { return (CBVH_SMEM_BOXES >> mode) & 1; }
 constexpr int kSurv = 64;  // exact-test queue entries per warp (pose, tri A, tri B)
 // per-warp shared memory: stack + leaf queue (+ the exact-test queue, distance only)
 __host__ __device__ constexpr int warp_smem_words(int mode, int kx) {
-  return nfields(kx) * kStack + 5 * kLeafQ + (mode == 1 ? 3 * kSurv : 0);
+  return nfields(kx) * kStack + 5 * kLeafQ + (mode == 1 ? 3 * kSurv : 0) + (smem_boxes(mode) ? 12 * 32 : 0);
 }
 
 // child pairs of an item: Alg. 1 enumerates children of every side it
@@ -1076,6 +1080,7 @@ struct WarpCtx {
   uint32_t* st;     // stack SoA [nfields(KX)][kStack]
   uint32_t* lq;     // leaf queue SoA [5][kLeafQ]: pose, topoA, topoB, triangle lists, lower bound (distance)
   uint32_t* sq;     // exact-test queue SoA [3][kSurv]: pose, triangle of A, triangle of B
+  uint32_t* scr;    // per-lane parking of the child boxes [12][32] (CBVH_SMEM_BOXES)
   uint32_t* spill;  // this warp's global spill area [kSpillCap][nfields(KX)]
   int lane;
 };
@@ -1367,6 +1372,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
   c.st = smem + wib * warp_smem_words(MODE, KX);
   c.lq = c.st + NF * kStack;
   c.sq = c.lq + 5 * kLeafQ;
+  c.scr = c.sq + (MODE == 1 ? 3 * kSurv : 0);
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * NF;
   int top = 0, nleaf = 0, spill_top = 0;
   int after = 0;  // iterations since the input ran out
@@ -1582,6 +1588,15 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
         float alo[3], ahi[3], blo[3], bhi[3];
         words_to_float(p.A, CA, alo, ahi);
         words_to_float(p.B, CB, blo, bhi);
+        if (smem_boxes(MODE)) {
+          // park the child boxes in shared memory across the tests: under
+          // register pressure the compiler spills them to local memory
+          #pragma unroll
+          for (int q = 0; q < 6; ++q) {
+            c.scr[q * 32 + c.lane] = (uint32_t)CA[q];
+            c.scr[(6 + q) * 32 + c.lane] = (uint32_t)CB[q];
+          }
+        }
         if (MODE == 0) {
           sg = sat_gap<false>(P, alo, ahi, blo, bhi, eps, nullptr);
           surv = sg <= 0.f;
@@ -1692,6 +1707,13 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
         if (push) {
           const int s2 = top + pos;
           CBVH_CHECK(p, s2 < kStack);
+          if (smem_boxes(MODE)) {
+            #pragma unroll
+            for (int q = 0; q < 6; ++q) {
+              CA[q] = (int32_t)c.scr[q * 32 + c.lane];
+              CB[q] = (int32_t)c.scr[(6 + q) * 32 + c.lane];
+            }
+          }
           c.st[F_POSE * kStack + s2] = pose | descent_flags(p.descent, cta, ctb, CA, CB, p.A, p.B);
           c.st[F_TA * kStack + s2] = cta;
           c.st[F_TB * kStack + s2] = ctb;
