@@ -915,6 +915,9 @@ __device__ __noinline__ float tri_dist_fp64(const PoseF& P, const float* trisA, 
 // the traversal kernel
 // ----------------------------------------------------------------------------
 
+#ifndef CBVH_LATE_LOADS
+#define CBVH_LATE_LOADS 1
+#endif
 #ifndef CBVH_SMEM_BOXES
 #define CBVH_SMEM_BOXES 2  // bit 0: collide, bit 1: distance (measured: distance config 4 -6 %, collide +1.5..2 %)
 #endif
@@ -1278,11 +1281,11 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
   return tests;
 }
 
-// Move the bottom half of the smem stack to the warp's global spill area.
-// Returns the new (top, spill_top); on overflow flags CBVH_EOVERFLOW.
+// Move the bottom H entries (default half the stack, at most `top`) of the
+// smem stack to the warp's global spill area.  Returns the new (top,
+// spill_top); on overflow flags CBVH_EOVERFLOW.
 template <int NF>
-__device__ __noinline__ int2 spill_out(const Params& p, const WarpCtx c, int top, int spill_top) {
-  constexpr int H = kStack / 2;
+__device__ __noinline__ int2 spill_out(const Params& p, const WarpCtx c, int top, int spill_top, int H = kStack / 2) {
   if (spill_top + H > kSpillCap) {
     if (c.lane == 0) atomicExch(&p.ctl->error, (unsigned)(-CBVH_EOVERFLOW));
     return make_int2(0, spill_top);  // abandon; cbvh_check reports the error
@@ -1501,6 +1504,15 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     unsigned starts;
     if (n0 > 32) {  // B = 8, both internal: one item in two passes
       m = 1; total = n0; passes = (n0 + 31) >> 5; starts = 1u;
+#if CBVH_LATE_LOADS
+      // the item stays on the stack during its passes (its boxes are read
+      // where they are decoded), so make room for both passes' pushes first
+      if (top + 32 * passes > kStack) {
+        int2 r = spill_out<NF>(p, c, top, spill_top, top + 32 * passes - kStack);
+        top = r.x; spill_top = r.y;
+        if (top == 0) continue;  // spill area full: the error is flagged, the item abandoned
+      }
+#endif
     } else {
       const unsigned fit = __ballot_sync(FULL, c.lane < top && incl <= 32);
       m = __popc(fit);
@@ -1516,6 +1528,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     const uint32_t pose = pword & kPoseMask;
     const uint32_t ta = c.st[F_TA * kStack + slot];
     const uint32_t tb = c.st[F_TB * kStack + slot];
+#if !CBVH_LATE_LOADS
     int32_t BA[6], BB[6], BX[2 * KX + 1];
     #pragma unroll
     for (int q = 0; q < 6; ++q) {
@@ -1524,19 +1537,23 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     }
     #pragma unroll
     for (int q = 0; q < 2 * KX; ++q) BX[q] = (int32_t)c.st[(F_XB + q) * kStack + slot];
+#endif
     // leaf masks in bits 0-7; distance: the lower bound's float bits above
     // (rounded down to a multiple of 256 ulp)
     const uint32_t item_w = c.st[F_LB * kStack + slot];
     const float item_lb = __uint_as_float(item_w & ~0xFFu);
     __syncwarp();
-    top -= m;
+    const bool hold = CBVH_LATE_LOADS && passes > 1;
+    if (!hold) top -= m;
     if (STATS) { s_exp += m; s_iter += passes; }
 
     CBVH_CHECK(p, pose < (uint32_t)p.N && slot >= 0 && slot < kStack);
+#if !CBVH_LATE_LOADS
     const PoseF P = load_pose(p.poses, (int)pose);
-    const bool early_done = MODE == 0 && p.early_exit && __ldcg(&p.hit[pose]) != 0;
     const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
     const float eps = 2e-6f * (tmax + scale_ab);
+#endif
+    const bool early_done = MODE == 0 && p.early_exit && __ldcg(&p.hit[pose]) != 0;
     float best = FLT_MAX;
     if (MODE == 1) best = __uint_as_float(__ldcg(&p.dist_bits[pose]));
     const bool a_int = (pword & kDescA) != 0, b_int = (pword & kDescB) != 0;  // sides descended
@@ -1563,7 +1580,27 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
         if (!b_int) mskB = (item_w >> 4) & 15u;
       }
       bool bad = false;  // checked build: an out-of-range child drops the lane
+#if CBVH_LATE_LOADS
+      // the pose and the item's parent boxes are loaded where they are used
+      // (short live ranges: at the register cap they were spilled to local
+      // memory across the pop bookkeeping); the item's slot is intact — the
+      // pushes of this pass come after the __syncwarp below, and a held
+      // multi-pass item is not popped until its last pass
+      const PoseF P = load_pose(p.poses, (int)pose);
+      const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
+      const float eps = 2e-6f * (tmax + scale_ab);
+      int32_t BA[6], BB[6], BX[2 * KX + 1];
+#endif
       if (valid) {
+#if CBVH_LATE_LOADS
+        #pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          BA[q] = (int32_t)c.st[(F_BA + q) * kStack + slot];
+          BB[q] = (int32_t)c.st[(F_BB + q) * kStack + slot];
+        }
+        #pragma unroll
+        for (int q = 0; q < 2 * KX; ++q) BX[q] = (int32_t)c.st[(F_XB + q) * kStack + slot];
+#endif
         if (a_int) {
           uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
           CBVH_GUARD(p, node < p.A.n_nodes, (node = 0, bad = true));
@@ -1674,6 +1711,9 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       const bool leafpair = surv && (cta & kLeafBit) && (ctb & kLeafBit);
       const bool push = surv && !leafpair;
       // ---- ballot/popc compaction: internal pairs back onto the stack
+#if CBVH_LATE_LOADS
+      __syncwarp();  // every lane has read its item before any push lands on it
+#endif
       const unsigned pm = __ballot_sync(FULL, push);
       if (pm) {
         if (top + 32 > kStack) {
@@ -1756,6 +1796,13 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
         s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
         nleaf = 0;
       }
+    }
+    if (hold) {
+      // pop the held multi-pass item: the top entry moves into its slot
+      if (top - 1 != slot)
+        for (int f = c.lane; f < NF; f += 32) c.st[f * kStack + slot] = c.st[f * kStack + top - 1];
+      __syncwarp();
+      top -= 1;
     }
     if (MODE == 1 && nleaf > 0 && top == 0) {
       s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
