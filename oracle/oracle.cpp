@@ -121,9 +121,87 @@ bool compute_interval(const double p[3], const double d[3], double* t0, double* 
   return true;
 }
 
+// ----------------------------------------------------------------------------
+// Degenerate (zero-area) triangles.  SPEC allows duplicate-position triangles
+// and requires the tests to fall back to segment / point logic.
+// A closed triangle with a zero normal is the convex hull of three collinear
+// points: the segment between its two farthest-apart vertices (a point when
+// all three coincide).
+// ----------------------------------------------------------------------------
+
+bool is_zero(const double* v) { return v[0] == 0 && v[1] == 0 && v[2] == 0; }
+
+void hull_segment(const double T[3][3], double a[3], double b[3]) {
+  int bi = 0, bj = 1;
+  double best = -1;
+  for (int i = 0; i < 3; ++i)
+    for (int j = i + 1; j < 3; ++j) {
+      double d[3];
+      sub(T[j], T[i], d);
+      if (dot(d, d) > best) { best = dot(d, d); bi = i; bj = j; }
+    }
+  for (int k = 0; k < 3; ++k) { a[k] = T[bi][k]; b[k] = T[bj][k]; }
+}
+
+// Drop the dominant axis of the normal N: the two remaining coordinates.
+void plane_axes(const double* N, int* i0, int* i1) {
+  double a0 = std::fabs(N[0]), a1 = std::fabs(N[1]), a2 = std::fabs(N[2]);
+  if (a0 >= a1 && a0 >= a2) { *i0 = 1; *i1 = 2; }
+  else if (a1 >= a2) { *i0 = 0; *i1 = 2; }
+  else { *i0 = 0; *i1 = 1; }
+}
+
+double point_segment_dist2(const double* p, const double* a, const double* b);
+double segment_segment_dist2(const double* p0, const double* p1, const double* q0, const double* q1);
+
+// Closed segment ab against a non-degenerate closed triangle U with normal N.
+bool segment_triangle_intersect(const double* a, const double* b, const double U[3][3], const double* N) {
+  double wa[3], wb[3];
+  sub(a, U[0], wa); sub(b, U[0], wb);
+  const double da = dot(N, wa), db = dot(N, wb);  // signed plane offsets (units of |N|)
+  if ((da > 0 && db > 0) || (da < 0 && db < 0)) return false;
+  int i0, i1;
+  plane_axes(N, &i0, &i1);
+  double u[3][2];
+  for (int k = 0; k < 3; ++k) { u[k][0] = U[k][i0]; u[k][1] = U[k][i1]; }
+  if (da == 0 && db == 0) {
+    // the segment lies in U's plane: it meets U iff it crosses an edge or
+    // an endpoint lies inside
+    double pa[2] = {a[i0], a[i1]}, pb[2] = {b[i0], b[i1]};
+    for (int j = 0; j < 3; ++j)
+      if (segments_intersect_2d(pa, pb, u[j], u[(j + 1) % 3])) return true;
+    return point_in_tri_2d(pa, u[0], u[1], u[2]);
+  }
+  // a single crossing point p = a + t (b - a), t = da / (da - db) in [0, 1]
+  const double t = da / (da - db);
+  double p2[2] = {a[i0] + t * (b[i0] - a[i0]), a[i1] + t * (b[i1] - a[i1])};
+  return point_in_tri_2d(p2, u[0], u[1], u[2]);
+}
+
+bool tri_tri_intersect_degenerate(const double V[3][3], const double U[3][3], const double* N1, const double* N2) {
+  double a[3], b[3], c[3], d[3];
+  if (is_zero(N1) && is_zero(N2)) {
+    // two segments (or points): closed sets meet iff their distance is zero
+    hull_segment(V, a, b);
+    hull_segment(U, c, d);
+    return segment_segment_dist2(a, b, c, d) == 0.0;
+  }
+  if (is_zero(N1)) {
+    hull_segment(V, a, b);
+    return segment_triangle_intersect(a, b, U, N2);
+  }
+  hull_segment(U, a, b);
+  return segment_triangle_intersect(a, b, V, N1);
+}
+
 bool tri_tri_intersect(const double V[3][3], const double U[3][3]) {
   double e1[3], e2[3], N1[3], N2[3];
   sub(V[1], V[0], e1); sub(V[2], V[0], e2); cross(e1, e2, N1);
+  {
+    double f1[3], f2[3];
+    sub(U[1], U[0], f1); sub(U[2], U[0], f2); cross(f1, f2, N2);
+    if (is_zero(N1) || is_zero(N2)) return tri_tri_intersect_degenerate(V, U, N1, N2);
+  }
   double d1 = -dot(N1, V[0]);
   double du[3];
   for (int k = 0; k < 3; ++k) du[k] = dot(N1, U[k]) + d1;
