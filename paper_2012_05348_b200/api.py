@@ -123,6 +123,31 @@ def _check_poses(poses):
     return int(poses.shape[0])
 
 
+def _check_out(name, t, N, dtypes, device):
+    """Caller-supplied output buffer: the kernels write N elements through its pointer."""
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or t.dtype not in dtypes:
+        raise TypeError(f"{name} must be a tensor of dtype {' or '.join(map(str, dtypes))}")
+    if t.device != device or not t.is_contiguous() or t.numel() < N:
+        raise ValueError(f"{name} must be contiguous with >= {N} elements on {device}")
+
+
+def _check_bvh(T: "CompressedBVH", device):
+    if T.bound is None or T.device_blob is None:
+        raise ValueError("CompressedBVH is not on a device: call .to_device() first")
+    if T.device_blob.device != device:
+        raise ValueError(f"blob is on {T.device_blob.device}, poses on {device}")
+
+
+def _temp_workspace(A, B, mode, device, stream):
+    """A call-local workspace, allocated on the call's stream so the caching
+    allocator does not hand its memory out while the kernels still run."""
+    torch = _torch()
+    s = torch.cuda.current_stream(device) if stream is None else stream
+    with torch.cuda.stream(s):
+        return Workspace(A, B, mode, device)
+
+
 def validate_poses(poses, tol: float = 1e-6) -> np.ndarray:
     """Host-side pose check (R orthonormal within 1e-6; finite values).
 
@@ -151,21 +176,34 @@ def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=Non
     descent: "larger" (default: descend the node with the larger box) or
     "simultaneous" (Alg. 1 verbatim).  Both give identical results.
     early_exit: stop each pose at its first hit (planning only needs the
-    boolean); the hit flag is exact, the count a lower bound."""
+    boolean); the hit flag is exact, the count a lower bound.
+
+    Device errors (a traversal-stack overflow) land in the workspace's error
+    word: with a caller-supplied workspace, call ``check(workspace)`` after
+    the call (it synchronises); without one, this call checks before it
+    returns (and so synchronises the stream)."""
     torch = _torch()
     N = _check_poses(poses)
     dev = poses.device
-    if hit is None:
-        hit = torch.empty(N, dtype=torch.uint8, device=dev)
-    if count is None:
-        count = torch.empty(N, dtype=torch.int32, device=dev)
-    if workspace is None:
-        workspace = Workspace(A, B, 0, dev)
-    o = _opts(descent, stats, early_exit)
-    L.check(L.load().collide_batch_ex(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
-                                      C.c_void_p(hit.data_ptr()), C.c_void_p(count.data_ptr()),
-                                      C.c_void_p(workspace.ptr), workspace.nbytes,
-                                      C.c_void_p(_stream_ptr(stream)), C.byref(o)))
+    _check_bvh(A, dev)
+    _check_bvh(B, dev)
+    with torch.cuda.device(dev):
+        if hit is None:
+            hit = torch.empty(N, dtype=torch.uint8, device=dev)
+        if count is None:
+            count = torch.empty(N, dtype=torch.int32, device=dev)
+        _check_out("hit", hit, N, (torch.uint8, torch.bool), dev)
+        _check_out("count", count, N, (torch.int32, torch.uint32) if hasattr(torch, "uint32") else (torch.int32,), dev)
+        temp = workspace is None
+        if temp:
+            workspace = _temp_workspace(A, B, 0, dev, stream)
+        o = _opts(descent, stats, early_exit)
+        L.check(L.load().collide_batch_ex(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
+                                          C.c_void_p(hit.data_ptr()), C.c_void_p(count.data_ptr()),
+                                          C.c_void_p(workspace.ptr), workspace.nbytes,
+                                          C.c_void_p(_stream_ptr(stream)), C.byref(o)))
+        if temp:
+            check(workspace, stream)
     return hit, count
 
 
@@ -174,21 +212,31 @@ def distance_batch(A: CompressedBVH, B: CompressedBVH, poses, dist=None,
                    descent: str = "larger", caps=None):
     """C-ABI distance_batch: per-pose minimum triangle–triangle distance (fp32).
     caps (optional, fp32 [N] on the poses' device): per-pose caps — the result
-    is min(distance, cap), exact below the cap (cbvh_query_opts.capped)."""
+    is min(distance, cap), exact below the cap (cbvh_query_opts.capped).
+    Error checking as collide_batch."""
     torch = _torch()
     N = _check_poses(poses)
-    if dist is None:
-        dist = torch.empty(N, dtype=torch.float32, device=poses.device)
-    if caps is not None:
-        if caps.shape != (N,) or caps.dtype != torch.float32 or caps.device != poses.device:
-            raise ValueError("caps must be fp32 [N] on the poses' device")
-        dist.copy_(caps)
-    if workspace is None:
-        workspace = Workspace(A, B, 1, poses.device)
-    o = _opts(descent, stats, capped=caps is not None)
-    L.check(L.load().distance_batch_ex(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
-                                       C.c_void_p(dist.data_ptr()), C.c_void_p(workspace.ptr), workspace.nbytes,
-                                       C.c_void_p(_stream_ptr(stream)), C.byref(o)))
+    dev = poses.device
+    _check_bvh(A, dev)
+    _check_bvh(B, dev)
+    with torch.cuda.device(dev):
+        if dist is None:
+            dist = torch.empty(N, dtype=torch.float32, device=dev)
+        _check_out("dist", dist, N, (torch.float32,), dev)
+        if caps is not None:
+            if caps.shape != (N,) or caps.dtype != torch.float32 or caps.device != dev:
+                raise ValueError("caps must be fp32 [N] on the poses' device")
+            with torch.cuda.stream(torch.cuda.current_stream(dev) if stream is None else stream):
+                dist[:N].copy_(caps)
+        temp = workspace is None
+        if temp:
+            workspace = _temp_workspace(A, B, 1, dev, stream)
+        o = _opts(descent, stats, capped=caps is not None)
+        L.check(L.load().distance_batch_ex(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
+                                           C.c_void_p(dist.data_ptr()), C.c_void_p(workspace.ptr), workspace.nbytes,
+                                           C.c_void_p(_stream_ptr(stream)), C.byref(o)))
+        if temp:
+            check(workspace, stream)
     return dist
 
 

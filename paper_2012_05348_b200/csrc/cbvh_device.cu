@@ -36,6 +36,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <cfloat>
 #include <cmath>
 #include <cstddef>
@@ -1283,11 +1285,20 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
 
 // Move the bottom H entries (default half the stack, at most `top`) of the
 // smem stack to the warp's global spill area.  Returns the new (top,
-// spill_top); on overflow flags CBVH_EOVERFLOW.
-template <int NF>
+// spill_top).  On overflow the warp abandons its smem stack: it flags
+// CBVH_EOVERFLOW and marks every pose with an abandoned item conservatively —
+// collide: hit = 1 (the count stays a lower bound); distance: 0 — so a caller
+// that skips cbvh_check never sees a missed contact as a clear pose.
+template <int MODE, int NF>
 __device__ __noinline__ int2 spill_out(const Params& p, const WarpCtx c, int top, int spill_top, int H = kStack / 2) {
   if (spill_top + H > kSpillCap) {
     if (c.lane == 0) atomicExch(&p.ctl->error, (unsigned)(-CBVH_EOVERFLOW));
+    for (int e = c.lane; e < top; e += 32) {
+      const uint32_t pose = c.st[F_POSE * kStack + e] & kPoseMask;
+      if (MODE == 0) p.hit[pose] = 1;
+      else atomicMin(&p.dist_bits[pose], 0u);
+    }
+    __syncwarp();
     return make_int2(0, spill_top);  // abandon; cbvh_check reports the error
   }
   __syncwarp();
@@ -1508,7 +1519,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       // the item stays on the stack during its passes (its boxes are read
       // where they are decoded), so make room for both passes' pushes first
       if (top + 32 * passes > kStack) {
-        int2 r = spill_out<NF>(p, c, top, spill_top, top + 32 * passes - kStack);
+        int2 r = spill_out<MODE, NF>(p, c, top, spill_top, top + 32 * passes - kStack);
         top = r.x; spill_top = r.y;
         if (top == 0) continue;  // spill area full: the error is flagged, the item abandoned
       }
@@ -1717,7 +1728,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       const unsigned pm = __ballot_sync(FULL, push);
       if (pm) {
         if (top + 32 > kStack) {
-          int2 r = spill_out<NF>(p, c, top, spill_top);
+          int2 r = spill_out<MODE, NF>(p, c, top, spill_top);
           top = r.x; spill_top = r.y;
           if (STATS) s_spill++;
         }
@@ -1895,6 +1906,8 @@ struct LaunchShape {
   int warps;
 };
 
+constexpr int kMaxDevices = 64;
+
 template <int MODE, bool STATS, int KX>
 static int shape_for(LaunchShape* s) {
   int dev = 0, sms = 0, per_sm = 0;
@@ -1902,17 +1915,21 @@ static int shape_for(LaunchShape* s) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
-  static bool attr_set = false;
-  if (!attr_set) {
+  // the dynamic shared-memory opt-in and the occupancy are per device: cached
+  // per device (a race only repeats the idempotent calls)
+  static std::atomic<int> cached[kMaxDevices];
+  const int slot = dev < kMaxDevices ? dev : -1;
+  per_sm = slot >= 0 ? cached[slot].load(std::memory_order_acquire) : 0;
+  if (per_sm == 0) {
     e = cudaFuncSetAttribute(traverse_kernel<MODE, STATS, KX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem_bytes(MODE, KX));
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    attr_set = true;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel<MODE, STATS, KX>, kWarps * 32,
+                                                      smem_bytes(MODE, KX));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (per_sm < 1) per_sm = 1;
+    if (slot >= 0) cached[slot].store(per_sm, std::memory_order_release);
   }
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel<MODE, STATS, KX>, kWarps * 32,
-                                                    smem_bytes(MODE, KX));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-  if (per_sm < 1) per_sm = 1;
   s->blocks = sms * per_sm;
   s->warps = s->blocks * kWarps;
   return CBVH_OK;
@@ -1950,37 +1967,39 @@ static int extra_axes(const cbvh_bvh* B) { return B ? (int)B->h.kdop / 2 - 3 : 0
 // Greedy dive before a distance traversal (reading R26); CBVH_DIVE=0 turns it
 // off (A/B only).
 static bool dive_enabled() {
-  static int on = -1;
-  if (on < 0) {
+  static const bool on = [] {  // thread-safe one-time initialisation
     const char* env = std::getenv("CBVH_DIVE");
-    on = (env && *env) ? (std::atoi(env) != 0) : 1;
-  }
-  return on != 0;
+    return (env && *env) ? (std::atoi(env) != 0) : true;
+  }();
+  return on;
 }
 
 // Phase schedule: budgets of the bounded phases, then one
 // unbounded phase.  CBVH_PHASES="b0,b1,..." overrides (tuning only).
+struct PhaseSchedule {
+  int n = 0;
+  int b[kMaxPhases];
+};
 static int phase_budgets(int* out) {
-  static int n = -1;
-  static int b[kMaxPhases];
-  if (n < 0) {
-    n = 0;
+  static const PhaseSchedule sched = [] {  // thread-safe one-time initialisation
+    PhaseSchedule r;
     const char* env = std::getenv("CBVH_PHASES");
     if (env && *env) {
       const char* q = env;
-      while (*q && n < kMaxPhases - 1) {
-        b[n++] = std::atoi(q);
+      while (*q && r.n < kMaxPhases - 1) {
+        r.b[r.n++] = std::atoi(q);
         while (*q && *q != ',') ++q;
         if (*q == ',') ++q;
       }
     } else {
-      b[n++] = 32;
-      b[n++] = 32;
-      b[n++] = 64;
+      r.b[r.n++] = 32;
+      r.b[r.n++] = 32;
+      r.b[r.n++] = 64;
     }
-  }
-  for (int k = 0; k < n; ++k) out[k] = b[k];
-  return n;
+    return r;
+  }();
+  for (int k = 0; k < sched.n; ++k) out[k] = sched.b[k];
+  return sched.n;
 }
 
 static DevTree make_tree(const cbvh_bvh* T) {

@@ -128,6 +128,86 @@ __device__ __forceinline__ bool interval(const F p[3], const F d[3], F* t0, F* t
 }
 
 template <class F>
+__device__ F seg_seg_d2(const F* p0, const F* p1, const F* q0, const F* q1);
+template <class F>
+__device__ __forceinline__ F pt_seg_d2(const F* p, const F* a, const F* b);
+
+// ---- zero-area triangles.  SPEC allows duplicate-position triangles
+// and asks for segment / point fallbacks: a closed triangle whose
+// normal is the zero vector is the segment between its two farthest vertices
+// (a point when all coincide).  Reached only from the rare branches of
+// tri_tri_overlap where a normal has come out exactly zero.
+template <class F>
+__device__ __forceinline__ bool is_zero3(const F* n) { return n[0] == F(0) && n[1] == F(0) && n[2] == F(0); }
+
+template <class F>
+__device__ void far_pair(const TriT<F>& T, F a[3], F b[3]) {
+  F d01[3], d12[3], d20[3];
+  vsub(T.v[1], T.v[0], d01); vsub(T.v[2], T.v[1], d12); vsub(T.v[0], T.v[2], d20);
+  const F l01 = vdot(d01, d01), l12 = vdot(d12, d12), l20 = vdot(d20, d20);
+  const int i = (l01 >= l12 && l01 >= l20) ? 0 : (l12 >= l20 ? 1 : 2);
+  for (int k = 0; k < 3; ++k) { a[k] = T.v[i][k]; b[k] = T.v[(i + 1) % 3][k]; }
+}
+
+// Closed segment ab against the closed non-degenerate triangle T with normal
+// n.  Off the plane: the endpoints must not lie strictly on one side, and the
+// line through a, b must pass through the closed triangle — the triple
+// products (b - a) . ((t_i - a) x (t_i+1 - a)) share a sign (zeros allowed).
+// In the plane: 2-D edge crossings or an endpoint inside, on the coordinate
+// plane that drops n's dominant axis.
+template <class F>
+__device__ __noinline__ bool seg_tri_closed(const F* a, const F* b, const TriT<F>& T, const F* n) {
+  F wa[3], wb[3];
+  vsub(a, T.v[0], wa); vsub(b, T.v[0], wb);
+  const F sa = vdot(n, wa), sb = vdot(n, wb);
+  if ((sa > F(0) && sb > F(0)) || (sa < F(0) && sb < F(0))) return false;
+  if (sa == F(0) && sb == F(0)) {
+    const F ax = fabs(n[0]), ay = fabs(n[1]), az = fabs(n[2]);
+    const int j0 = (ax >= ay && ax >= az) ? 1 : 0, j1 = (az > ax && az > ay) ? 1 : 2;
+    const F p[2] = {a[j0], a[j1]}, q[2] = {b[j0], b[j1]};
+    F t[3][2];
+    for (int k = 0; k < 3; ++k) { t[k][0] = T.v[k][j0]; t[k][1] = T.v[k][j1]; }
+    for (int k = 0; k < 3; ++k)
+      if (seg2_intersect(p, q, t[k], t[(k + 1) % 3])) return true;
+    return pt_in_tri2(p, t[0], t[1], t[2]);
+  }
+  F d[3];
+  vsub(b, a, d);
+  bool neg = false, pos = false;
+  for (int k = 0; k < 3; ++k) {
+    F p[3], q[3], c[3];
+    vsub(T.v[k], a, p); vsub(T.v[(k + 1) % 3], a, q); vcross(p, q, c);
+    const F s = vdot(d, c);
+    neg = neg || s < F(0);
+    pos = pos || s > F(0);
+  }
+  return !(neg && pos);
+}
+
+template <class F>
+__device__ __noinline__ bool degenerate_overlap(const TriT<F>& V, const TriT<F>& U) {
+  F e1[3], e2[3], N1[3], N2[3], a[3], b[3];
+  vsub(V.v[1], V.v[0], e1); vsub(V.v[2], V.v[0], e2); vcross(e1, e2, N1);
+  vsub(U.v[1], U.v[0], e1); vsub(U.v[2], U.v[0], e2); vcross(e1, e2, N2);
+  if (is_zero3(N1) && is_zero3(N2)) {
+    // two segments (or points): they meet iff their distance is zero —
+    // the endpoint-to-segment terms and the interior stationary point
+    F c[3], d[3];
+    far_pair(V, a, b);
+    far_pair(U, c, d);
+    const F m = fmin(fmin(fmin(pt_seg_d2(a, c, d), pt_seg_d2(b, c, d)), fmin(pt_seg_d2(c, a, b), pt_seg_d2(d, a, b))),
+                     seg_seg_d2(a, b, c, d));
+    return m == F(0);
+  }
+  if (is_zero3(N1)) {
+    far_pair(V, a, b);
+    return seg_tri_closed(a, b, U, N2);
+  }
+  far_pair(U, a, b);
+  return seg_tri_closed(a, b, V, N1);
+}
+
+template <class F>
 __device__ bool tri_tri_overlap(const TriT<F>& V, const TriT<F>& U) {
   F e1[3], e2[3], N1[3], N2[3];
   vsub(V.v[1], V.v[0], e1); vsub(V.v[2], V.v[0], e2); vcross(e1, e2, N1);
@@ -138,14 +218,17 @@ __device__ bool tri_tri_overlap(const TriT<F>& V, const TriT<F>& U) {
   F d2 = -vdot(N2, U.v[0]);
   F dv[3] = {vdot(N2, V.v[0]) + d2, vdot(N2, V.v[1]) + d2, vdot(N2, V.v[2]) + d2};
   if ((dv[0] > 0 && dv[1] > 0 && dv[2] > 0) || (dv[0] < 0 && dv[1] < 0 && dv[2] < 0)) return false;
-  if (du[0] == 0 && du[1] == 0 && du[2] == 0) return coplanar2(N1, V, U);
+  // (a zero normal — a zero-area triangle — makes du or the line direction D
+  // vanish, so it can only arrive in these two branches)
+  if (du[0] == 0 && du[1] == 0 && du[2] == 0)
+    return (is_zero3(N1) || is_zero3(N2)) ? degenerate_overlap(V, U) : coplanar2(N1, V, U);
   F D[3];
   vcross(N1, N2, D);
   int ax = 0;
   F m = fabs(D[0]);
   if (fabs(D[1]) > m) { m = fabs(D[1]); ax = 1; }
   if (fabs(D[2]) > m) { m = fabs(D[2]); ax = 2; }
-  if (m == 0) return coplanar2(N1, V, U);
+  if (m == 0) return (is_zero3(N1) || is_zero3(N2)) ? degenerate_overlap(V, U) : coplanar2(N1, V, U);
   F vp[3] = {V.v[0][ax], V.v[1][ax], V.v[2][ax]};
   F up[3] = {U.v[0][ax], U.v[1][ax], U.v[2][ax]};
   F a0, a1, b0, b1;
