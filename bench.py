@@ -129,8 +129,22 @@ def aggregate_rate(units_per_rank: int, steps: int, world: int, seconds: float) 
     return units_per_rank * steps * world / seconds
 
 
-def cpu_oracle_rate(w, n_sample: int, nthreads: int = 0, budget_s: float = 25.0):
-    """The fp64 oracle (as it stands) on a bounded prefix of the workload's poses."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_oracle_rate(w, n_sample: int, nthreads: int = 0, budget_s: float = 25.0, distance: bool = False):
+    """The fp64 oracle (as it stands) on a bounded prefix of the workload's
+    poses.  Returns the rate and the oracle's per-pose answers for that prefix
+    (collide: count, H, Z; distance: d64) so the GPU's are checked against them."""
     import oracle as O
     t0 = time.time()
     tA = O.Tree.from_mesh(w.A.vertices, w.A.triangles)
@@ -140,19 +154,64 @@ def cpu_oracle_rate(w, n_sample: int, nthreads: int = 0, budget_s: float = 25.0)
     cores = nthreads or os.cpu_count()
     # grow the sample until ~budget_s of oracle time (bounded by n_sample)
     n, done, el = 64, 0, 0.0
+    parts = []
     while True:
         P = w.poses[done:done + n]
         t = time.time()
-        O.collide(tA, tB, P, delta, nthreads)
+        if distance:
+            d64, _ = O.distance(tA, tB, P, nthreads)
+            parts.append((d64,))
+        else:
+            cnt, H, Z, _ = O.collide(tA, tB, P, delta, nthreads)
+            parts.append((cnt, H, Z))
         el += time.time() - t
         done += len(P)
         if el > budget_s or done >= n_sample:
             break
         n = min(n_sample - done, max(64, int(len(P) * max(1.0, (budget_s - el) / max(el, 1e-3)) * 0.5)))
-    return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+    answers = tuple(np.concatenate([p[k] for p in parts]) for k in range(len(parts[0])))
+    return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"first {done} of {len(w.poses)} poses of {w.name}, fp64 oracle with "
                       f"std::thread x {cores}; oracle BVH build {build_s:.1f} s not timed",
-            "seconds": el}
+            "seconds": el, "poses": done, "answers": answers, "delta": delta}
+
+
+def bench_parity(cpu, hit, cnt, dst, distance: bool) -> dict:
+    """The GPU's answers of the timed run against the oracle's on the
+    cpu_baseline sample (tests/parity.py rules: band rule for counts, 1e-5
+    relative for distances)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from parity import check_collide, check_distance
+    n = cpu["poses"]
+    try:
+        if distance:
+            rep = check_distance(dst[:n].cpu().numpy(), cpu["answers"][0], cpu["delta"], "bench")
+        else:
+            _, H, Z = cpu["answers"]
+            rep = check_collide(hit[:n].cpu().numpy(), cnt[:n].cpu().numpy().view(np.uint32), H, Z, "bench")
+        rep["status"] = "ok"
+    except AssertionError as e:
+        rep = {"status": "FAIL", "error": str(e)[:300]}
+    rep["poses_checked"] = n
+    rep["rule"] = ("|gpu - d64| <= 1e-5 d64 (gpu <= 2 delta near contact)" if distance else
+                   "H <= count <= H + Z per pose; hit exact outside the band (Z = pairs with |s| <= delta)")
+    return rep
+
+
+def l2_peak() -> dict | None:
+    """Measured L2 read bandwidth (libcbvh_probe.so, csrc/probe_l2.cu)."""
+    import ctypes as C
+    path = os.path.join(ROOT, "paper_2012_05348_b200", "libcbvh_probe.so")
+    if not os.path.exists(path):
+        return None
+    lib = C.CDLL(path)
+    gbs, nb, l2 = C.c_double(0), C.c_size_t(0), C.c_size_t(0)
+    msg = C.create_string_buffer(256)
+    if lib.cbvh_probe_l2_read_gbs(C.byref(gbs), C.byref(nb), C.byref(l2), msg) != 0:
+        return None
+    return {"l2_read_gbs": gbs.value, "buffer_bytes": nb.value, "l2_bytes": l2.value,
+            "source": "measured in this run: csrc/probe_l2.cu, 16-B ld.global.cg stream over an "
+                      "L2-resident buffer (best of L2/8, L2/4, L2/2), CUDA events"}
 
 
 def run_reference(args):
@@ -183,7 +242,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": w.name, "poses_per_step": per_step,
                                             "sample": "consecutive pose windows of the config-5 batch"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": f"{per_step} poses per step x {args.steps} steps"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -343,9 +402,11 @@ def run(args):
             e2e_ms.append(a.elapsed_time(b))
     E = max_over_ranks(sum(e2e_ms) / 1e3, dist, dev)
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_oracle_rate(w, n_sample=args.cpu_poses, budget_s=args.cpu_budget)
+        cpu = cpu_oracle_rate(w, n_sample=args.cpu_poses, budget_s=args.cpu_budget, distance=distance)
+        parity = bench_parity(cpu, hit, cnt, dst, distance)
+    l2 = l2_peak() if rank == 0 else None
 
     if rank == 0:
         line = {
@@ -355,6 +416,9 @@ def run(args):
             "config": {"workload": w.name, "poses_per_gpu": N, "A_tris": w.A.num_triangles,
                        "B_tris": w.B.num_triangles, "branching": w.branching, "bits": w.bits,
                        "treelet_nodes": w.treelet, "leaf_size": w.leaf, "layout": args.layout, "kdop_B": args.kdop,
+                       "descent": args.descent + (" (one side per internal pair, DESIGN R15)" if args.descent == "larger"
+                                                  else " (Alg. 1 verbatim)"),
+                       "early_exit": bool(args.early_exit), "preset": args.preset,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"pose-sharded x{world} (independent batches)"},
             "bv_pair_tests_per_s": st["bv_tests"] / (statistics.median(step_ms) / 1e3),
@@ -367,11 +431,22 @@ def run(args):
             "bytes_per_node": {"A": A.info["bytes_per_node"], "B": B.info["bytes_per_node"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                         "traffic_source": (f"committed ncu capture {nc.get('source', 'profiles/ncu_traffic.json')}: "
+                                            "dram__bytes_read.sum + dram__bytes_write.sum per launch"
+                                            if traffic is not None else None),
                          "kernel": "traverse_kernel<%s> (all phases)" % ("distance" if distance else "collide"),
                          "kernel_ms": 1e3 * kern_s,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "peak_source": peaks["_source"] + " hbm_gbs (copy bandwidth)"},
+            "roofline_l2": ({"bound": "l2", "achieved": achieved, "peak": l2["l2_read_gbs"], "unit": "GB/s",
+                            "frac": achieved / l2["l2_read_gbs"], "kernel": "traverse_kernel (all phases)",
+                            "peak_source": l2["source"], "l2_bytes": l2["l2_bytes"],
+                            "probe_buffer_bytes": l2["buffer_bytes"],
+                            "note": "the same algorithmic bytes as roofline; the hierarchy and most "
+                                    "triangle records are L1/L2-resident, so this is the level they are "
+                                    "served from"} if l2 else None),
             "roofline_issue": issue,
+            "parity": parity,
             "stats": st,
             "e2e": {"value": aggregate_rate(N, args.steps, world, E), "unit": UNIT,
                     "h2d_bytes_per_step": int(poses_h.numel() * 4),
@@ -381,7 +456,8 @@ def run(args):
             "build_s": build_s,
         }
         if cpu is not None:
-            line["cpu_baseline"] = {k: v for k, v in cpu.items() if k != "seconds"}
+            line["cpu_baseline"] = {k: v for k, v in cpu.items() if k in ("value", "unit", "cores", "kind", "sample",
+                                                                          "cpu_model")}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -110,6 +110,14 @@ struct Builder {
 
 inline int bitlen64(int64_t x) { int n = 0; while (x > 0) { ++n; x >>= 1; } return n; }
 
+// Smallest lattice exponent whose cell 2^e is at least 2^-30 of |origin|, so
+// origin + k 2^e moves with every k in fp64 (and the lattice search loops
+// terminate) even for a zero-extent mesh.
+inline int min_cell_exp(double origin_abs) {
+  if (!(origin_abs > 0)) return -100;
+  return std::max(-100, std::ilogb(origin_abs) - 30);
+}
+
 template <class X> void put(std::vector<uint8_t>& buf, size_t off, X x) { std::memcpy(&buf[off], &x, sizeof(X)); }
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -197,6 +205,11 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   e = std::max(-100, std::min(100, e));
   while (std::ldexp(ext, -e) > double(1 << 22)) ++e;  // guard log2 rounding
   float origin[3] = {(float)root.lo[0], (float)root.lo[1], (float)root.lo[2]};
+  // the cell must stay resolvable next to the origin (origin + k 2^e distinct
+  // in fp64): a mesh whose extent is tiny or zero against its distance from
+  // 0 (a point, a sliver far out) gets a coarser lattice instead of a cell
+  // below the origin's ulp
+  e = std::max(e, min_cell_exp(std::max(std::fabs(origin[0]), std::max(std::fabs(origin[1]), std::fabs(origin[2])))));
   // x - origin can round in fp64 when |x| << |origin| (e.g. x ~ 1e-17), so
   // the floor/ceil estimate is corrected until origin + k 2^e (exact in fp64
   // for these magnitudes) lies on the conservative side of x.
@@ -293,6 +306,7 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
       int ea = ex > 0 ? (int)std::ceil(std::log2(ex)) - 22 : -100;
       ea = std::max(-100, std::min(100, ea));
       while (std::ldexp(ex, -ea) > double(1 << 22)) ++ea;
+      ea = std::max(ea, min_cell_exp(std::fabs(o)));
       xorigin[a] = o;
       xexp[a] = ea;
       auto at = [&](int64_t k) { return (double)o + std::ldexp((double)k, ea); };

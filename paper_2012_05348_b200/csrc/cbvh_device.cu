@@ -119,6 +119,13 @@ constexpr int kGrabItems = 1;       // continuation items acquired per cursor at
 #ifndef CBVH_LOW_WATER
 #define CBVH_LOW_WATER 4
 #endif
+#ifndef CBVH_POLL
+#define CBVH_POLL 1
+#endif
+#ifndef CBVH_POLL_EVERY
+#define CBVH_POLL_EVERY 32
+#endif
+constexpr unsigned kPoll = CBVH_POLL_EVERY;  // iterations between polls of the input cursor (power of two)
 constexpr int kGrab = CBVH_GRAB;          // poses acquired per cursor atomic
 constexpr int kLowWater = CBVH_LOW_WATER; // acquire poses when the stack is below this
 
@@ -891,6 +898,18 @@ __device__ __forceinline__ float tri_axis_gap(const Tri& V, const Tri& U) {
   return (umin - vmax) * rsqrtf(L2);
 }
 
+// The rare cases of Möller's test (coplanar or touching planes, zero-area
+// triangles) for triangle pair (ia, ib) under pose `pose`: the triangles are
+// re-read and re-mapped (bit-identical to the caller's copies) rather than
+// passed by reference, so the common register path never writes them to
+// local memory.
+__device__ __noinline__ bool overlap_rare(const Params& p, uint32_t pose, uint32_t ia, uint32_t ib) {
+  const PoseF P = load_pose(p.poses, (int)pose);
+  const Tri TA = load_tri(p.A.tris, ia);
+  const Tri TB = to_local(P, load_tri(p.B.tris, ib));
+  return tri_tri_overlap(TA, TB);
+}
+
 // fp64 re-evaluation of a near-contact distance candidate,
 // in the world frame as the distance is defined: A's fp32
 // triangle mapped by the fp32 pose lifted exactly to fp64, B's fp32 triangle
@@ -968,7 +987,10 @@ __device__ __forceinline__ uint32_t full_mask(uint32_t t) { return (2u << ((t >>
 // re-evaluated in fp64.
 __device__ __forceinline__ float pair_distance(const Params& p, const PoseF& P, const Tri& TA, const Tri& TB,
                                                uint32_t ia, uint32_t ib) {
-  float d = tri_tri_dist(TA, TB);
+  // a pair the fp32 register test finds intersecting, or cannot decide there
+  // (coplanar / zero-area), counts as distance 0 here and so is settled by the
+  // fp64 re-evaluation below, which runs the complete test
+  float d = moller_fast(TA, TB) != 0 ? 0.f : tri_tri_dist_disjoint(TA, TB);
   const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
   if (d < 0.05f * (tmax + p.A.maxabs + p.B.maxabs)) d = tri_dist_fp64(P, p.A.tris, ia, p.B.tris, ib);
   return d;
@@ -1114,7 +1136,8 @@ __device__ __forceinline__ void exact_batch(const Params& p, const WarpCtx c, in
     const Tri TA = load_tri(p.A.tris, ia);
     const Tri TB = to_local(P, load_tri(p.B.tris, ib));
     if (MODE == 0) {
-      hit = tri_tri_overlap(TA, TB);
+      const int r = moller_fast(TA, TB);
+      hit = r > 0 || (r < 0 && overlap_rare(p, pose, ia, ib));
     } else {
       d = pair_distance(p, P, TA, TB, ia, ib);
     }
@@ -1221,7 +1244,10 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
         // ~30 % SIMT it recovers for this cheaper test).
         const bool cand = !CBVH_DRAIN_AABB || tri_boxes_overlap(TA, TB);
         if (STATS && cand) ++*exact;
-        hit = cand && tri_tri_overlap(TA, TB);
+        if (cand) {
+          const int r = moller_fast(TA, TB);
+          hit = r > 0 || (r < 0 && overlap_rare(p, my_pose, ia, ib));
+        }
       } else {
         // triangle AABB gap: a lower bound; skip pairs that cannot beat the best
         const float tmax0 = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
@@ -1390,6 +1416,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * NF;
   int top = 0, nleaf = 0, spill_top = 0;
   int after = 0;  // iterations since the input ran out
+  unsigned poll = 0;  // iterations since the last exhaustion poll
   unsigned long long s_dump = 0, s_iter = 0, s_exact = 0;
   unsigned long long s_bv = 0, s_exp = 0, s_leaf = 0, s_tri = 0, s_dec = 0, s_rec = 0, s_lbytes = 0, s_spill = 0;
   bool poses_left = true;
@@ -1482,6 +1509,21 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       }
       if (poses_left) continue;
       break;
+    }
+    // ---- every warp learns when the input runs out, not only the warps that
+    // try to acquire: a warp deep in a heavy traversal polls the cursor every
+    // kPoll iterations (one L2 load by lane 0), so its budget starts and its
+    // backlog moves to the next phase with everybody else's
+    if (CBVH_POLL && poses_left && p.budget >= 0 && (++poll & (kPoll - 1)) == 0) {
+      unsigned cur = 0, lim = 0;
+      if (c.lane == 0) {
+        cur = __ldcg(&p.ctl->cursor[p.phase]);
+        lim = p.phase == 0 ? (unsigned)p.N : __ldcg(&p.ctl->count[p.phase - 1]);
+      }
+      if (__shfl_sync(FULL, cur >= lim ? 1 : 0, 0)) {
+        poses_left = false;
+        if (STATS && c.lane == 0 && p.phase == 0) atomicMin(&p.ctl->t_exhausted, globaltimer_ns());
+      }
     }
     // ---- bounded work after the input ran out: hand the rest to the next phase
     if (!poses_left && p.budget >= 0 && ++after > p.budget) {

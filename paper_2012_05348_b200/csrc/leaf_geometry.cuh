@@ -207,33 +207,52 @@ __device__ __noinline__ bool degenerate_overlap(const TriT<F>& V, const TriT<F>&
   return seg_tri_closed(a, b, V, N1);
 }
 
+// Möller's test in registers.  Returns 1 / 0 for the generic case, or -1
+// when the planes are coplanar or parallel-touching, or a normal is zero —
+// the rare cases tri_tri_overlap settles out of line.  The projections on the
+// dominant axis of the intersection line are selects, not a run-time index,
+// so neither triangle is ever written to local memory on this path.
 template <class F>
-__device__ bool tri_tri_overlap(const TriT<F>& V, const TriT<F>& U) {
+__device__ __forceinline__ int moller_fast(const TriT<F>& V, const TriT<F>& U) {
   F e1[3], e2[3], N1[3], N2[3];
   vsub(V.v[1], V.v[0], e1); vsub(V.v[2], V.v[0], e2); vcross(e1, e2, N1);
   F d1 = -vdot(N1, V.v[0]);
   F du[3] = {vdot(N1, U.v[0]) + d1, vdot(N1, U.v[1]) + d1, vdot(N1, U.v[2]) + d1};
-  if ((du[0] > 0 && du[1] > 0 && du[2] > 0) || (du[0] < 0 && du[1] < 0 && du[2] < 0)) return false;
+  if ((du[0] > 0 && du[1] > 0 && du[2] > 0) || (du[0] < 0 && du[1] < 0 && du[2] < 0)) return 0;
   vsub(U.v[1], U.v[0], e1); vsub(U.v[2], U.v[0], e2); vcross(e1, e2, N2);
   F d2 = -vdot(N2, U.v[0]);
   F dv[3] = {vdot(N2, V.v[0]) + d2, vdot(N2, V.v[1]) + d2, vdot(N2, V.v[2]) + d2};
-  if ((dv[0] > 0 && dv[1] > 0 && dv[2] > 0) || (dv[0] < 0 && dv[1] < 0 && dv[2] < 0)) return false;
-  // (a zero normal — a zero-area triangle — makes du or the line direction D
-  // vanish, so it can only arrive in these two branches)
-  if (du[0] == 0 && du[1] == 0 && du[2] == 0)
-    return (is_zero3(N1) || is_zero3(N2)) ? degenerate_overlap(V, U) : coplanar2(N1, V, U);
+  if ((dv[0] > 0 && dv[1] > 0 && dv[2] > 0) || (dv[0] < 0 && dv[1] < 0 && dv[2] < 0)) return 0;
+  if (du[0] == 0 && du[1] == 0 && du[2] == 0) return -1;
   F D[3];
   vcross(N1, N2, D);
-  int ax = 0;
-  F m = fabs(D[0]);
-  if (fabs(D[1]) > m) { m = fabs(D[1]); ax = 1; }
-  if (fabs(D[2]) > m) { m = fabs(D[2]); ax = 2; }
-  if (m == 0) return (is_zero3(N1) || is_zero3(N2)) ? degenerate_overlap(V, U) : coplanar2(N1, V, U);
-  F vp[3] = {V.v[0][ax], V.v[1][ax], V.v[2][ax]};
-  F up[3] = {U.v[0][ax], U.v[1][ax], U.v[2][ax]};
+  const F m0 = fabs(D[0]), m1 = fabs(D[1]), m2 = fabs(D[2]);
+  const bool x1 = m1 > m0, x2 = m2 > (x1 ? m1 : m0);  // dominant axis: 2 if x2, else 1 if x1, else 0
+  if ((x2 ? m2 : (x1 ? m1 : m0)) == 0) return -1;
+  F vp[3], up[3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    vp[k] = x2 ? V.v[k][2] : (x1 ? V.v[k][1] : V.v[k][0]);
+    up[k] = x2 ? U.v[k][2] : (x1 ? U.v[k][1] : U.v[k][0]);
+  }
   F a0, a1, b0, b1;
-  if (!interval(vp, dv, &a0, &a1) || !interval(up, du, &b0, &b1)) return coplanar2(N1, V, U);
-  return !(a1 < b0 || b1 < a0);
+  if (!interval(vp, dv, &a0, &a1) || !interval(up, du, &b0, &b1)) return -1;
+  return !(a1 < b0 || b1 < a0) ? 1 : 0;
+}
+
+// The complete test (closed triangles): the register path, then
+// the coplanar 2-D tests or the zero-area fallback.
+template <class F>
+__device__ bool tri_tri_overlap(const TriT<F>& V, const TriT<F>& U) {
+  const int r = moller_fast(V, U);
+  if (r >= 0) return r != 0;
+  F e1[3], e2[3], N1[3], N2[3];
+  vsub(V.v[1], V.v[0], e1); vsub(V.v[2], V.v[0], e2); vcross(e1, e2, N1);
+  vsub(U.v[1], U.v[0], e1); vsub(U.v[2], U.v[0], e2); vcross(e1, e2, N2);
+  // a zero normal (a zero-area triangle) makes du or the line direction
+  // vanish, so it arrives here; otherwise the planes coincide or touch
+  if (is_zero3(N1) || is_zero3(N2)) return degenerate_overlap(V, U);
+  return coplanar2(N1, V, U);
 }
 
 template <class F>
@@ -298,9 +317,10 @@ __device__ F pt_tri_d2(const F* p, const TriT<F>& T) {
   return fmin(fmin(pt_seg_d2(p, T.v[0], T.v[1]), pt_seg_d2(p, T.v[1], T.v[2])), pt_seg_d2(p, T.v[2], T.v[0]));
 }
 
+// Distance of two triangles already known not to intersect: the minimum over
+// the 6 vertex-triangle and 9 edge-edge terms.
 template <class F>
-__device__ F tri_tri_dist(const TriT<F>& V, const TriT<F>& U) {
-  if (tri_tri_overlap(V, U)) return F(0);
+__device__ F tri_tri_dist_disjoint(const TriT<F>& V, const TriT<F>& U) {
   F best = F(FLT_MAX);
   #pragma unroll 1
   for (int k = 0; k < 3; ++k) {
@@ -313,6 +333,12 @@ __device__ F tri_tri_dist(const TriT<F>& V, const TriT<F>& U) {
     for (int j = 0; j < 3; ++j)
       best = fmin(best, seg_seg_d2(V.v[i], V.v[(i + 1) % 3], U.v[j], U.v[(j + 1) % 3]));
   return sqrt_(best);
+}
+
+template <class F>
+__device__ F tri_tri_dist(const TriT<F>& V, const TriT<F>& U) {
+  if (tri_tri_overlap(V, U)) return F(0);
+  return tri_tri_dist_disjoint(V, U);
 }
 
 }  // namespace cbvh

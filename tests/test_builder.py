@@ -197,6 +197,31 @@ def test_compression_invariance_and_cost(cfg1, B, bits):
     assert st_dec[0] >= st_ex[0]
 
 
+@pytest.mark.parametrize("kdop", [6, 14])
+def test_degenerate_meshes_build(kdop):
+    # zero-area triangles are kept: a point, a sliver, a tiny triangle
+    # far from the origin and a flat mesh all build (the lattice search used to
+    # loop forever on a zero-extent root) and pass the independent checker
+    T1 = np.array([[0, 1, 2]], np.int32)
+    cases = [np.array([[0.25, 0.25, 0]] * 3, np.float32),
+             np.array([[2, 0, 0], [3, 0, 0], [4, 0, 0]], np.float32),
+             np.array([[1000, 1000, 1000], [1000, 1000, 1000.0001], [1000, 1000.0001, 1000]], np.float32),
+             np.zeros((3, 3), np.float32)]
+    for V in cases:
+        for B in (2, 4):
+            bv = M.build_compressed_bvh(V, T1, B, 8, kdop=kdop if B == 4 else 6)
+            assert O.check_blob(bv.blob, V, T1)["violations"] == 0
+    rng = np.random.default_rng(5)
+    V = rng.uniform(-1, 1, (60, 3)).astype(np.float32)
+    V[:, 2] = 0  # flat: zero extent in z
+    T = rng.integers(0, 60, (40, 3)).astype(np.int32)
+    # duplicate-position (not duplicate-index) triangles: zero area
+    T[:5, 1] = (T[:5, 0] + 1) % 60
+    V[T[:5, 1]] = V[T[:5, 0]]
+    bv = M.build_compressed_bvh(V, T, 4, 8, kdop=kdop)
+    assert O.check_blob(bv.blob, V, T)["violations"] == 0
+
+
 def test_error_paths():
     lib = L.load()
     V = np.zeros((3, 3), np.float32)

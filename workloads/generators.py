@@ -32,6 +32,7 @@ from __future__ import annotations
 
 import functools
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -186,6 +187,36 @@ def contact_poses(rng: np.random.Generator, n: int, centre_distance: float) -> n
     return pack_poses(quat_to_matrix(q), centre_distance * d)
 
 
+def zero_pose_draws(k: int, n: int, pose_seed_offset: int = 0):
+    """Rotations (fp64 [n,3,3]) and unit translation directions (fp64 [n,3])
+    of the zero-separation preset of config k: the config's pose seed,
+    standard_normal((n, 4)) quaternions, then standard_normal((n, 3))
+    directions (the same draws as contact_poses).  The magnitudes come from
+    the bisection table tools/make_zero_preset.py writes with the oracle."""
+    rng = np.random.default_rng(seeds(k)[2] + pose_seed_offset)
+    q = rng.standard_normal((n, 4))
+    d = rng.standard_normal((n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return quat_to_matrix(q), d
+
+
+PRESET_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "presets")
+
+
+def zero_poses(k: int, n: int | None = None) -> np.ndarray:
+    """The paper's "distance of zero" preset: per
+    pose a uniform rotation and direction, translated by the magnitude the
+    oracle's bisection found (0 < oracle distance < 1e-3), from
+    presets/zero_cfg{k}.npz (tools/make_zero_preset.py)."""
+    tab = np.load(os.path.join(PRESET_DIR, f"zero_cfg{k}.npz"))
+    s = tab["s"]
+    n = len(s) if n is None else int(n)
+    if n > len(s):
+        raise ValueError(f"the zero preset of config {k} has {len(s)} poses")
+    R, u = zero_pose_draws(k, len(s))
+    return pack_poses(R[:n], s[:n, None] * u[:n])
+
+
 def ring_poses(rng: np.random.Generator, n: int, major: float = 3.0,
                rho_lo: float = 4.5, rho_hi: float = 6.0) -> np.ndarray:
     """Config 4: A's centre at distance rho ~ U[4.5,6] from the torus ring (reading #19)."""
@@ -251,18 +282,22 @@ def make_config(k: int, num_poses: int | None = None, pose_seed_offset: int = 0,
     order only when num_poses is None). ``pose_seed_offset`` gives each rank of
     a multi-GPU run its own independent batch (weak scaling).
     ``preset="contact"`` (configs 1 and 3: two radius-1 spheres) replaces the
-    poses by the zero-distance preset (centres 2 apart, ``contact_poses``).
+    poses by the analytic near-contact preset (centres 2 apart,
+    ``contact_poses``); ``preset="zero"`` by the zero-separation preset found
+    by bisection with the oracle (``zero_poses``: 0 < distance < 1e-3 for
+    every pose; 1,024 poses for config 1, 32,768 for config 3).
     """
     sa, sb, sp = seeds(k)
     sp += pose_seed_offset
     n = CONFIG_POSES[k] if num_poses is None else int(num_poses)
     ra, rb, rp = (np.random.default_rng(s) for s in (sa, sb, sp))
-    if preset not in ("random", "contact") or (preset == "contact" and k not in (1, 3)):
-        raise ValueError("preset 'contact' is defined for configs 1 and 3 (two unit spheres)")
+    if preset not in ("random", "contact", "zero") or (preset != "random" and k not in (1, 3)):
+        raise ValueError("presets 'contact' and 'zero' are defined for configs 1 and 3 (two unit spheres)")
     if k == 1:
         A = _mesh(*noisy_sphere(ra, 32, 16))
         B = _mesh(*noisy_sphere(rb, 32, 16))
-        P = random_poses(rp, n, 2.5) if preset == "random" else contact_poses(rp, n, 2.0)
+        P = (random_poses(rp, n, 2.5) if preset == "random" else contact_poses(rp, n, 2.0) if preset == "contact"
+             else zero_poses(k, num_poses))
         return Workload(CONFIG_NAMES[k], A, B, P, branching=2, bits=8, treelet=32)
     if k == 2:
         A = _mesh(*noisy_sphere(ra, 64, 32))
@@ -272,7 +307,8 @@ def make_config(k: int, num_poses: int | None = None, pose_seed_offset: int = 0,
     if k == 3:
         A = _mesh(*noisy_sphere(ra, 128, 64))
         B = _mesh(*noisy_sphere(rb, 128, 64))
-        P = random_poses(rp, n, 2.5) if preset == "random" else contact_poses(rp, n, 2.0)
+        P = (random_poses(rp, n, 2.5) if preset == "random" else contact_poses(rp, n, 2.0) if preset == "contact"
+             else zero_poses(k, num_poses))
         settings = [(br, bi) for br in (2, 4, 8) for bi in (4, 8, 16)]
         return Workload(CONFIG_NAMES[k], A, B, P, branching=4, bits=8, treelet=32,
                         settings=settings)
