@@ -987,10 +987,7 @@ __device__ __forceinline__ uint32_t full_mask(uint32_t t) { return (2u << ((t >>
 // re-evaluated in fp64.
 __device__ __forceinline__ float pair_distance(const Params& p, const PoseF& P, const Tri& TA, const Tri& TB,
                                                uint32_t ia, uint32_t ib) {
-  // a pair the fp32 register test finds intersecting, or cannot decide there
-  // (coplanar / zero-area), counts as distance 0 here and so is settled by the
-  // fp64 re-evaluation below, which runs the complete test
-  float d = moller_fast(TA, TB) != 0 ? 0.f : tri_tri_dist_disjoint(TA, TB);
+  float d = tri_tri_dist(TA, TB);
   const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
   if (d < 0.05f * (tmax + p.A.maxabs + p.B.maxabs)) d = tri_dist_fp64(P, p.A.tris, ia, p.B.tris, ib);
   return d;
@@ -1415,8 +1412,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
   c.scr = c.sq + (MODE == 1 ? 3 * kSurv : 0);
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * NF;
   int top = 0, nleaf = 0, spill_top = 0;
-  int after = 0;  // iterations since the input ran out
-  unsigned poll = 0;  // iterations since the last exhaustion poll
+  int after = 0;  // iterations since the input ran out (before that: the poll counter)
   unsigned long long s_dump = 0, s_iter = 0, s_exact = 0;
   unsigned long long s_bv = 0, s_exp = 0, s_leaf = 0, s_tri = 0, s_dec = 0, s_rec = 0, s_lbytes = 0, s_spill = 0;
   bool poses_left = true;
@@ -1447,6 +1443,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
         }
         if (base >= (unsigned)p.N) {
           poses_left = false;
+          after = 0;
           if (STATS && c.lane == 0) atomicMin(&p.ctl->t_exhausted, globaltimer_ns());
         } else {
           const int k = min((int)g, p.N - (int)base);
@@ -1490,6 +1487,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
         base = __shfl_sync(FULL, base, 0);
         if (base >= avail) {
           poses_left = false;
+          after = 0;
         } else {
           const int k = min(kGrabItems, (int)(avail - base));
           for (int idx = c.lane; idx < k * NF; idx += 32) {
@@ -1514,7 +1512,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     // try to acquire: a warp deep in a heavy traversal polls the cursor every
     // kPoll iterations (one L2 load by lane 0), so its budget starts and its
     // backlog moves to the next phase with everybody else's
-    if (CBVH_POLL && poses_left && p.budget >= 0 && (++poll & (kPoll - 1)) == 0) {
+    if (CBVH_POLL && poses_left && p.budget >= 0 && (++after & (kPoll - 1)) == 0) {
       unsigned cur = 0, lim = 0;
       if (c.lane == 0) {
         cur = __ldcg(&p.ctl->cursor[p.phase]);
@@ -1522,6 +1520,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       }
       if (__shfl_sync(FULL, cur >= lim ? 1 : 0, 0)) {
         poses_left = false;
+        after = 0;
         if (STATS && c.lane == 0 && p.phase == 0) atomicMin(&p.ctl->t_exhausted, globaltimer_ns());
       }
     }

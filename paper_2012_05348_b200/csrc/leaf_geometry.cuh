@@ -240,19 +240,38 @@ __device__ __forceinline__ int moller_fast(const TriT<F>& V, const TriT<F>& U) {
   return !(a1 < b0 || b1 < a0) ? 1 : 0;
 }
 
-// The complete test (closed triangles): the register path, then
-// the coplanar 2-D tests or the zero-area fallback.
+// The complete test (closed triangles), as one function: the
+// distance variant's (fp32 and fp64) and the collide rare path's.  The
+// generic case is the same arithmetic as moller_fast; the coplanar and
+// zero-area cases branch off where the plane test and the line direction
+// vanish.
 template <class F>
 __device__ bool tri_tri_overlap(const TriT<F>& V, const TriT<F>& U) {
-  const int r = moller_fast(V, U);
-  if (r >= 0) return r != 0;
   F e1[3], e2[3], N1[3], N2[3];
   vsub(V.v[1], V.v[0], e1); vsub(V.v[2], V.v[0], e2); vcross(e1, e2, N1);
+  F d1 = -vdot(N1, V.v[0]);
+  F du[3] = {vdot(N1, U.v[0]) + d1, vdot(N1, U.v[1]) + d1, vdot(N1, U.v[2]) + d1};
+  if ((du[0] > 0 && du[1] > 0 && du[2] > 0) || (du[0] < 0 && du[1] < 0 && du[2] < 0)) return false;
   vsub(U.v[1], U.v[0], e1); vsub(U.v[2], U.v[0], e2); vcross(e1, e2, N2);
-  // a zero normal (a zero-area triangle) makes du or the line direction
-  // vanish, so it arrives here; otherwise the planes coincide or touch
-  if (is_zero3(N1) || is_zero3(N2)) return degenerate_overlap(V, U);
-  return coplanar2(N1, V, U);
+  F d2 = -vdot(N2, U.v[0]);
+  F dv[3] = {vdot(N2, V.v[0]) + d2, vdot(N2, V.v[1]) + d2, vdot(N2, V.v[2]) + d2};
+  if ((dv[0] > 0 && dv[1] > 0 && dv[2] > 0) || (dv[0] < 0 && dv[1] < 0 && dv[2] < 0)) return false;
+  // (a zero normal — a zero-area triangle — makes du or the line direction D
+  // vanish, so it can only arrive in these two branches)
+  if (du[0] == 0 && du[1] == 0 && du[2] == 0)
+    return (is_zero3(N1) || is_zero3(N2)) ? degenerate_overlap(V, U) : coplanar2(N1, V, U);
+  F D[3];
+  vcross(N1, N2, D);
+  int ax = 0;
+  F m = fabs(D[0]);
+  if (fabs(D[1]) > m) { m = fabs(D[1]); ax = 1; }
+  if (fabs(D[2]) > m) { m = fabs(D[2]); ax = 2; }
+  if (m == 0) return (is_zero3(N1) || is_zero3(N2)) ? degenerate_overlap(V, U) : coplanar2(N1, V, U);
+  F vp[3] = {V.v[0][ax], V.v[1][ax], V.v[2][ax]};
+  F up[3] = {U.v[0][ax], U.v[1][ax], U.v[2][ax]};
+  F a0, a1, b0, b1;
+  if (!interval(vp, dv, &a0, &a1) || !interval(up, du, &b0, &b1)) return coplanar2(N1, V, U);
+  return !(a1 < b0 || b1 < a0);
 }
 
 template <class F>
