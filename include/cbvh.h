@@ -69,6 +69,11 @@ typedef struct {
   int layout;        /* CBVH_LAYOUT_*; default CBVH_LAYOUT_DELTA (bits is ignored for FP16 / FP32) */
   int kdop;          /* k of the k-DOP bounding volumes (Table I): 0 or 6 = AABB (default), 14, 18, 26;
                         k > 6 requires CBVH_LAYOUT_DELTA and is supported for the static model B */
+  int align_treelets; /* non-zero: whole treelets are packed next-fit into T-slot blocks (node id = block T +
+                        offset; no treelet straddles a block; unused slots are padding), so a treelet block
+                        is one aligned, fixed-size span of the topology and code arrays that the traversal
+                        can stage in shared memory.  Needs the delta AABB layout and a
+                        power-of-two T in [4, 64] */
 } cbvh_build_opts;
 
 /* Build the compressed BVH of one mesh ("splitting the models and wrap it
@@ -100,7 +105,12 @@ typedef struct {
   uint32_t layout;     /* CBVH_LAYOUT_* */
   uint32_t kdop;       /* 6 (AABB) or 14 / 18 / 26 */
   uint64_t off_axes;   /* k-DOP axis table: per extra axis {fp32 origin, int32 exp, int32 root lo, root hi} */
+  uint32_t flags;      /* CBVH_FLAG_* */
+  uint32_t real_nodes; /* nodes of the tree (num_nodes counts node slots, padding included) */
 } cbvh_header;
+
+/* cbvh_header.flags */
+enum { CBVH_FLAG_ALIGNED_TREELETS = 1 };
 
 typedef struct {
   cbvh_header h;

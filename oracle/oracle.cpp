@@ -406,8 +406,14 @@ struct BlobView {
   uint32_t layout;  // 0 delta (lattice corrections), 1 absolute binary16, 2 absolute fp32
   uint32_t kdop;    // 6 (AABB) or 14 / 18 / 26: k/2 slab axes per node
   uint64_t off_axes;
+  uint32_t flags;       // bit 0: aligned treelets — treelet k owns node slots [k T, k T + T)
+  uint32_t real_nodes;  // nodes of the tree; n_nodes counts slots (padding included)
   uint32_t nax() const { return kdop / 2; }
+  bool aligned() const { return flags & 1u; }
 };
+
+// Topology word of an unused (padding) slot of an aligned treelet.
+constexpr uint32_t kPadSlot = 0x7FFFFFFFu;
 
 template <class X> X rd(const uint8_t* p, size_t off) { X x; std::memcpy(&x, p + off, sizeof(X)); return x; }
 
@@ -425,6 +431,11 @@ bool parse_blob(const uint8_t* p, size_t bytes, BlobView* b) {
   b->layout = rd<uint32_t>(p, 136);
   b->kdop = rd<uint32_t>(p, 140);
   b->off_axes = rd<uint64_t>(p, 144);
+  b->flags = rd<uint32_t>(p, 152);
+  b->real_nodes = rd<uint32_t>(p, 156);
+  if (b->flags > 1u || b->real_nodes == 0 || b->real_nodes > b->n_nodes) return false;
+  if (!b->aligned() && b->real_nodes != b->n_nodes) return false;
+  if (b->aligned() && b->n_nodes % b->T != 0) return false;
   if (b->kdop != 6 && b->kdop != 14 && b->kdop != 18 && b->kdop != 26) return false;
   if (b->total != bytes) return false;
   if (b->layout == 0 && b->w != 4 && b->w != 8 && b->w != 16) return false;
@@ -1007,7 +1018,15 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
       }
     }
   }
-  for (uint32_t n = 0; n < b.n_nodes; ++n) if (!seen[n]) report[0]++;
+  // every slot is reached, except (aligned treelets) padding slots, which
+  // must hold the padding word and zero codes
+  uint64_t reached = 0;
+  for (uint32_t n = 0; n < b.n_nodes; ++n) {
+    if (seen[n]) { ++reached; continue; }
+    if (!b.aligned() || blob_topo(b, n) != kPadSlot) { report[0]++; continue; }
+    for (uint32_t f = 0; f < 2 * b.nax(); ++f) if (code_field(b, n, f) != 0) report[0]++;
+  }
+  if (reached != b.real_nodes) report[0]++;
   // subtree triangle sets, bottom-up (reverse DFS preorder), then containment
   for (auto it = order.rbegin(); it != order.rend(); ++it) {
     uint32_t n = *it;
@@ -1040,7 +1059,14 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
     int32_t anchor[6];
     for (int a = 0; a < 6; ++a) anchor[a] = rd<int32_t>(b.p, o + 4 * a);
     uint32_t first = rd<uint32_t>(b.p, o + 24), cnt = rd<uint32_t>(b.p, o + 28);
-    if (first != expect_first || cnt == 0) report[5]++;
+    // contiguous ranges in order; aligned: a treelet that would straddle a
+    // T-slot block boundary starts the next block instead (the slots skipped
+    // are padding, checked above), and none straddles one
+    const uint64_t next_block = (expect_first + b.T - 1) / b.T * b.T;
+    const bool placed = first == expect_first ||
+                        (b.aligned() && first == next_block && expect_first % b.T + cnt > b.T);
+    if (!placed || cnt == 0) report[5]++;
+    if (b.aligned() && cnt > 0 && first / b.T != (first + cnt - 1) / b.T) report[5]++;
     if (cnt > b.T) report[6]++;
     expect_first = (uint64_t)first + cnt;
     if ((uint64_t)first + cnt > b.n_nodes) { report[5]++; continue; }
@@ -1059,7 +1085,8 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
       if (anchor[a] != want) report[7]++;
     }
   }
-  if (expect_first != b.n_nodes) report[5]++;
+  if (b.aligned() ? (expect_first > b.n_nodes || b.n_nodes - expect_first >= b.T) : expect_first != b.n_nodes)
+    report[5]++;
   // k-DOP slab axes (layout 0 only): decode every extra axis top-down (DFS
   // preorder has parents first), then check child-in-parent and containment of
   // the exact projections of each subtree's vertices (bottom-up).

@@ -172,6 +172,9 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   if (kdop != 6 && layout != CBVH_LAYOUT_DELTA) return set_error(CBVH_EINVAL, "k-DOPs use the delta layout");
   if (layout != CBVH_LAYOUT_DELTA && layout != CBVH_LAYOUT_FP16 && layout != CBVH_LAYOUT_FP32)
     return set_error(CBVH_EINVAL, "layout must be CBVH_LAYOUT_DELTA, _FP16 or _FP32");
+  const bool aligned = opts && opts->align_treelets;
+  if (aligned && (T < 4 || T > 64 || (T & (T - 1)) || layout != CBVH_LAYOUT_DELTA || kdop != 6))
+    return set_error(CBVH_EINVAL, "align_treelets needs the delta AABB layout and a power-of-two T in [4, 64]");
   if (!mesh->vertices || !mesh->triangles) return set_error(CBVH_EINVAL, "null mesh arrays");
   const int64_t nv = mesh->num_vertices, nt = mesh->num_triangles;
   if (nt <= 0 || nv <= 0) return set_error(CBVH_EMESH, "empty mesh");
@@ -379,14 +382,35 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
     treelets.push_back(tl);
   }
 
+  // aligned treelets: whole treelets are packed next-fit, in creation order,
+  // into T-slot blocks (node id = block * T + offset); a treelet never
+  // straddles a block boundary and the slots a block does not fill are
+  // padding.  A block is the unit the traversal stages in shared memory.
+  int nslots = n;
+  if (aligned) {
+    int fill = 0, block = 0;
+    for (auto& tl : treelets) {
+      if (fill + tl.count > T) { ++block; fill = 0; }
+      const int first = block * T + fill;
+      for (int j = 0; j < tl.count; ++j) new_id[order[tl.first + j]] = first + j;
+      tl.first = first;
+      fill += tl.count;
+    }
+    nslots = (block + 1) * T;
+  }
+  // node id -> original node (-1: a padding slot)
+  std::vector<int> slot_node(nslots, -1);
+  for (int x = 0; x < n; ++x) slot_node[new_id[x]] = x;
+
   // ---- triangle soup in leaf order of the new numbering
-  std::vector<uint32_t> topo(n), tri_index;
+  std::vector<uint32_t> topo(nslots, kPadTopo), tri_index;
   std::vector<float> soup;
   tri_index.reserve(nt);
   soup.reserve(12 * (size_t)nt);
   int depth = 0, leaves = 0;
-  for (int nid = 0; nid < n; ++nid) {
-    const BNode& nd = bd.nodes[order[nid]];
+  for (int nid = 0; nid < nslots; ++nid) {
+    if (slot_node[nid] < 0) continue;
+    const BNode& nd = bd.nodes[slot_node[nid]];
     depth = std::max(depth, nd.depth);
     if (nd.children.empty()) {
       ++leaves;
@@ -452,8 +476,8 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   const int nax = kdop / 2;
   const size_t code_bytes_node = 2 * (size_t)nax * w / 8;
   size_t off_topo = 256;
-  size_t off_codes = align256(off_topo + 4 * (size_t)n);
-  size_t off_axes = align256(off_codes + code_bytes_node * (size_t)n);
+  size_t off_codes = align256(off_topo + 4 * (size_t)nslots);
+  size_t off_axes = align256(off_codes + code_bytes_node * (size_t)nslots);
   size_t off_treelets = align256(off_axes + 16 * (size_t)nx);
   size_t off_tris = align256(off_treelets + 32 * treelets.size());
   size_t off_tri_index = align256(off_tris + 48 * (size_t)nt);
@@ -470,7 +494,7 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   put<uint32_t>(out, 16, (uint32_t)T);
   put<uint32_t>(out, 20, (uint32_t)c);
   put<uint32_t>(out, 24, w);
-  put<uint32_t>(out, 28, (uint32_t)n);
+  put<uint32_t>(out, 28, (uint32_t)nslots);
   put<uint32_t>(out, 32, (uint32_t)nt);
   put<uint32_t>(out, 36, (uint32_t)treelets.size());
   put<uint32_t>(out, 40, (uint32_t)depth);
@@ -487,6 +511,8 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   put<uint32_t>(out, 136, (uint32_t)layout);
   put<uint32_t>(out, 140, (uint32_t)kdop);
   put<uint64_t>(out, 144, off_axes);
+  put<uint32_t>(out, 152, aligned ? CBVH_FLAG_ALIGNED_TREELETS : 0u);
+  put<uint32_t>(out, 156, (uint32_t)n);
   for (int a = 0; a < nx; ++a) {
     const size_t o = off_axes + 16 * (size_t)a;
     put<float>(out, o, xorigin[a]);
@@ -494,11 +520,13 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
     put<int32_t>(out, o + 8, (int32_t)xroot[2 * a]);
     put<int32_t>(out, o + 12, (int32_t)xroot[2 * a + 1]);
   }
-  std::memcpy(&out[off_topo], topo.data(), 4 * (size_t)n);
-  for (int nid = 0; nid < n; ++nid) {
-    const uint16_t* q = &code[6 * (size_t)order[nid]];
+  std::memcpy(&out[off_topo], topo.data(), 4 * (size_t)nslots);
+  for (int nid = 0; nid < nslots; ++nid) {
+    if (slot_node[nid] < 0) continue;  // padding: zero codes
+    const int on = slot_node[nid];
+    const uint16_t* q = &code[6 * (size_t)on];
     uint8_t* dst = &out[off_codes + code_bytes_node * nid];
-    const BNode& nd = bd.nodes[order[nid]];
+    const BNode& nd = bd.nodes[on];
     if (layout == CBVH_LAYOUT_FP32) {
       // absolute boxes: min/max of fp32 coordinates are fp32 values (exact)
       for (int a = 0; a < 3; ++a) {
@@ -519,8 +547,8 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
       std::vector<uint32_t> f(2 * (size_t)nax);
       for (int a = 0; a < 3; ++a) { f[a] = q[a]; f[nax + a] = q[3 + a]; }
       for (int a = 0; a < nx; ++a) {
-        f[3 + a] = (uint32_t)xcode_v[((size_t)a * n + order[nid]) * 2];
-        f[nax + 3 + a] = (uint32_t)xcode_v[((size_t)a * n + order[nid]) * 2 + 1];
+        f[3 + a] = (uint32_t)xcode_v[((size_t)a * n + on) * 2];
+        f[nax + 3 + a] = (uint32_t)xcode_v[((size_t)a * n + on) * 2 + 1];
       }
       if (w == 16) {
         for (size_t k = 0; k < f.size(); ++k) { const uint16_t v = (uint16_t)f[k]; std::memcpy(dst + 2 * k, &v, 2); }
@@ -552,6 +580,9 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
   if (h->layout > 2) return set_error(CBVH_EBLOB, "bad layout");
   h->kdop = u32(140);
   h->off_axes = u64(144);
+  h->flags = u32(152);
+  h->real_nodes = u32(156);
+  if (h->flags & ~(uint32_t)CBVH_FLAG_ALIGNED_TREELETS) return set_error(CBVH_EBLOB, "unknown header flags");
   if (h->kdop != 6 && h->kdop != 14 && h->kdop != 18 && h->kdop != 26) return set_error(CBVH_EBLOB, "bad k");
   if (h->kdop != 6 && h->layout != CBVH_LAYOUT_DELTA) return set_error(CBVH_EBLOB, "k-DOP with an absolute layout");
   h->branching = u32(8); h->bits = u32(12); h->treelet_nodes = u32(16); h->leaf_size = u32(20);
@@ -578,6 +609,13 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
       h->off_tri_index + 4ull * h->num_tris > h->total_bytes)
     return set_error(CBVH_EBLOB, "bad section offsets");
   if ((h->off_topo | h->off_codes | h->off_tris) & 15) return set_error(CBVH_EBLOB, "misaligned sections");
+  if (h->real_nodes == 0 || h->real_nodes > h->num_nodes) return set_error(CBVH_EBLOB, "bad node count");
+  if ((h->flags & CBVH_FLAG_ALIGNED_TREELETS) &&
+      (h->treelet_nodes > 64 || (h->treelet_nodes & (h->treelet_nodes - 1)) || h->layout != CBVH_LAYOUT_DELTA ||
+       h->kdop != 6 || h->num_nodes % h->treelet_nodes != 0))
+    return set_error(CBVH_EBLOB, "bad aligned-treelet layout");
+  if (!(h->flags & CBVH_FLAG_ALIGNED_TREELETS) && h->real_nodes != h->num_nodes)
+    return set_error(CBVH_EBLOB, "bad node count");
   return CBVH_OK;
 }
 
@@ -614,10 +652,13 @@ int cbvh_blob_info(const uint8_t* h_blob, size_t bytes, cbvh_info* out) {
   int rc = cbvh::parse_header(h_blob, bytes, &out->h);
   if (rc) return rc;
   const cbvh_header& h = out->h;
-  out->bvh_bytes = 4ull * h.num_nodes + ((uint64_t)h.kdop * h.code_width / 8) * h.num_nodes + 32ull * h.num_treelets +
-                   16ull * (h.kdop / 2 - 3);
+  // the hierarchy the traversal reads: topology words and codes of every node
+  // slot (aligned treelets include their padding slots) and the k-DOP axis
+  // table; the treelet table (anchors) is build metadata the device never
+  // reads, so it is not counted
+  out->bvh_bytes = 4ull * h.num_nodes + ((uint64_t)h.kdop * h.code_width / 8) * h.num_nodes + 16ull * (h.kdop / 2 - 3);
   out->tri_bytes = 48ull * h.num_tris;
-  out->bytes_per_node = (double)out->bvh_bytes / (double)h.num_nodes;
+  out->bytes_per_node = (double)out->bvh_bytes / (double)h.real_nodes;
   out->code_bytes_per_node = (double)h.kdop * h.code_width / 8.0;
   return CBVH_OK;
 }

@@ -123,7 +123,7 @@ constexpr int kGrabItems = 1;       // continuation items acquired per cursor at
 #define CBVH_POLL 1
 #endif
 #ifndef CBVH_POLL_EVERY
-#define CBVH_POLL_EVERY 32
+#define CBVH_POLL_EVERY 128
 #endif
 constexpr unsigned kPoll = CBVH_POLL_EVERY;  // iterations between polls of the input cursor (power of two)
 constexpr int kGrab = CBVH_GRAB;          // poses acquired per cursor atomic
@@ -2189,9 +2189,13 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
   const char* skip = std::getenv("CBVH_SKIP_BLOB_VALIDATION");
   if (!(skip && skip[0] == '1')) {
     const uint8_t* tp = h_blob + h.off_topo;
+    auto topo_at = [&](uint64_t n) { uint32_t w; std::memcpy(&w, tp + 4ull * n, 4); return w; };
+    const bool padded = (h.flags & CBVH_FLAG_ALIGNED_TREELETS) != 0;
+    uint64_t real = 0;
     for (uint32_t n = 0; n < h.num_nodes; ++n) {
-      uint32_t w;
-      std::memcpy(&w, tp + 4ull * n, 4);
+      const uint32_t w = topo_at(n);
+      if (padded && w == kPadTopo) continue;  // padding slot: checked unreferenced below
+      ++real;
       if (w & kLeafBit) {
         const uint64_t first = w & 0x1FFFFFFFu, cnt = ((w >> 29) & 3u) + 1;
         if (first + cnt > h.num_tris || cnt > h.leaf_size) return set_error(CBVH_EBLOB, "bad leaf triangle range");
@@ -2199,8 +2203,12 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
         const uint64_t first = w & 0x0FFFFFFFu, cnt = ((w >> 28) & 7u) + 1;
         if (first <= n || first + cnt > h.num_nodes || cnt < 2 || cnt > h.branching)
           return set_error(CBVH_EBLOB, "bad child range");
+        if (padded)
+          for (uint64_t k = first; k < first + cnt; ++k)
+            if (topo_at(k) == kPadTopo) return set_error(CBVH_EBLOB, "child in a padding slot");
       }
     }
+    if (real != h.real_nodes || (padded && topo_at(0) == kPadTopo)) return set_error(CBVH_EBLOB, "bad node count");
   }
   std::memset(out, 0, sizeof *out);
   out->d_blob = d_blob;

@@ -22,5 +22,7 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h);
 //   leaf:     bit 31 = 1, bits 29..30 = ntri - 1, bits 0..28 = first triangle
 //   internal: bit 31 = 0, bits 28..30 = nchild - 1, bits 0..27 = first child
 constexpr uint32_t kLeafBit = 0x80000000u;
+// topology word of a padding slot of an aligned treelet (never referenced)
+constexpr uint32_t kPadTopo = 0x7FFFFFFFu;
 
 }  // namespace cbvh

@@ -85,6 +85,55 @@ def test_invariants_16k(mesh16k, B, bits, T):
     assert r["violations"] == 0, r
 
 
+@pytest.mark.parametrize("B,bits,T", [(2, 8, 32), (4, 8, 32), (4, 8, 64), (8, 16, 64), (4, 4, 16)])
+def test_aligned_treelets(cfg1, mesh16k, B, bits, T):
+    # align_treelets: whole treelets packed next-fit into T-slot blocks; the padding
+    # slots are unreachable and zero, the decoded boxes and the pair sets are
+    # those of the packed numbering (independent checker + traversal)
+    for m in (cfg1.A, mesh16k):
+        al = M.build_compressed_bvh(m.vertices, m.triangles, B, bits, T, 4, align_treelets=True)
+        pk = M.build_compressed_bvh(m.vertices, m.triangles, B, bits, T, 4)
+        r = O.check_blob(al.blob, m.vertices, m.triangles)
+        assert r["violations"] == 0, r
+        i = al.info
+        assert i["aligned_treelets"] and i["num_nodes"] % T == 0 and i["num_nodes"] >= i["real_nodes"]
+        assert i["real_nodes"] == pk.info["num_nodes"] == r["nodes_checked"]
+        assert i["num_treelets"] == pk.info["num_treelets"]
+        topo_al = np.frombuffer(al.blob[i["off_topo"]:i["off_topo"] + 4 * i["num_nodes"]].tobytes(), np.uint32)
+        assert np.count_nonzero(topo_al == 0x7FFFFFFF) == i["num_nodes"] - i["real_nodes"]
+    A, Bm, P = cfg1.A, cfg1.B, cfg1.poses[:24]
+    ta = O.Tree.from_blob(M.build_compressed_bvh(A.vertices, A.triangles, B, bits, T, 4, align_treelets=True).blob,
+                          A.vertices, A.triangles)
+    tb = O.Tree.from_blob(M.build_compressed_bvh(Bm.vertices, Bm.triangles, B, bits, T, 4, align_treelets=True).blob,
+                          Bm.vertices, Bm.triangles)
+    ra, rb = O.Tree.from_mesh(A.vertices, A.triangles), O.Tree.from_mesh(Bm.vertices, Bm.triangles)
+    for p in P:
+        assert O.collide_pairs(ta, tb, p) == O.collide_pairs(ra, rb, p)
+
+
+def test_aligned_treelets_errors_and_faults(cfg1):
+    A = cfg1.A
+    for kw in (dict(treelet_nodes=48), dict(treelet_nodes=128), dict(layout="fp32"), dict(kdop=14)):
+        with pytest.raises(L.CbvhError, match="EINVAL"):
+            M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, align_treelets=True, **kw)
+    bv = M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, 32, 4, align_treelets=True)
+    i = bv.info
+    topo = np.frombuffer(bv.blob[i["off_topo"]:i["off_topo"] + 4 * i["num_nodes"]].tobytes(), np.uint32)
+    pad = int(np.nonzero(topo == 0x7FFFFFFF)[0][0])
+    # a padding slot holding a code, or a parent pointing into padding, is caught
+    bad = bv.blob.copy()
+    bad[i["off_codes"] + 6 * pad] = 3
+    assert O.check_blob(bad, A.vertices, A.triangles)["malformed"] > 0
+    lib = L.load()
+    out = L.cbvh_bvh()
+    internal = int(np.nonzero((topo >> 31) == 0)[0][1])
+    bad = bv.blob.copy()
+    w = (int(topo[internal]) & ~0x0FFFFFFF) | (pad - 1)
+    bad[i["off_topo"] + 4 * internal:i["off_topo"] + 4 * internal + 4] = np.frombuffer(np.uint32(w).tobytes(), np.uint8)
+    rc = lib.cbvh_bind(bad.ctypes.data_as(C.POINTER(C.c_uint8)), bad.nbytes, C.c_void_p(1 << 20), C.byref(out))
+    assert rc == L.CBVH_EBLOB
+
+
 def test_node_counts_closed_form(cfg1):
     # equal-count median split, c = 4: a binary tree over 960 triangles has
     # 2 * 256 - 1 = 511 nodes (960 / 4 = 240 leaves -> padded split shape)
