@@ -273,9 +273,10 @@ def run(args):
         w.branching = args.branching
     if args.bits:
         w.bits = args.bits
-    A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout)
+    A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout,
+                               align_treelets=args.align_treelets)
     B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout,
-                               kdop=args.kdop)
+                               kdop=args.kdop, align_treelets=args.align_treelets)
     distance = (w.mode if args.mode == "auto" else args.mode) == "distance"
     build_s = time.time() - t0
     A.to_device(dev)
@@ -292,10 +293,10 @@ def run(args):
 
     def step(stats=False):
         if distance:
-            M.distance_batch(A, B, poses, dst, ws, stats=stats, descent=args.descent)
+            M.distance_batch(A, B, poses, dst, ws, stats=stats, descent=args.descent, staging=args.staging)
         else:
             M.collide_batch(A, B, poses, hit, cnt, ws, stats=stats, descent=args.descent,
-                            early_exit=args.early_exit)
+                            early_exit=args.early_exit, staging=args.staging)
 
     # ---- first (cold) call, then warm-up (untimed by the contract; the cold
     # call's own time is reported as cold_first_call_ms)
@@ -350,6 +351,8 @@ def run(args):
                               "dumped": st["dumped"], "launches": M.last_launch_count(),
                               "timeline_ms": [t / 1e6 for t in st["timeline_ns"]],
                               "lane_util": st["bv_tests"] / max(1, 32 * st["iterations"]),
+                              "treelet_blocks": st["treelet_blocks"], "staged_reads": st["staged_reads"],
+                              "nodes_decoded": st["nodes_decoded"],
                               "iterations": st["iterations"], "bv_tests": st["bv_tests"], "leaf_pairs": st["leaf_pairs"], "tri_tests": st["tri_tests"], "exact_tests": st["exact_tests"], "layout": args.layout, "kdop": args.kdop, "early_exit": args.early_exit,
                               "bytes_per_node": {"A": A.info["bytes_per_node"], "B": B.info["bytes_per_node"]}}), flush=True)
         return
@@ -419,6 +422,7 @@ def run(args):
                        "descent": args.descent + (" (one side per internal pair, DESIGN R15)" if args.descent == "larger"
                                                   else " (Alg. 1 verbatim)"),
                        "early_exit": bool(args.early_exit), "preset": args.preset,
+                       "align_treelets": bool(args.align_treelets), "staging": args.staging,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"pose-sharded x{world} (independent batches)"},
             "bv_pair_tests_per_s": st["bv_tests"] / (statistics.median(step_ms) / 1e3),
@@ -477,8 +481,9 @@ def main():
     ap.add_argument("--leaf", type=int, default=0, help="override the leaf size c (1..4)")
     ap.add_argument("--bits", type=int, default=0, help="override b (config-3 sweep)")
     ap.add_argument("--descent", default="larger", choices=["larger", "simultaneous"])
-    ap.add_argument("--preset", default="random", choices=["random", "contact"],
-                    help="pose preset; 'contact' = the paper's zero-distance preset (configs 1, 3)")
+    ap.add_argument("--preset", default="random", choices=["random", "contact", "zero"],
+                    help="pose preset (configs 1, 3): 'zero' = the paper's zero-distance preset by bisection "
+                         "(oracle distance in (0, 1e-3)), 'contact' = centres 2 apart")
     ap.add_argument("--early-exit", action="store_true",
                     help="hit-only collide (stop each pose at its first hit); not the headline metric")
     ap.add_argument("--mode", default="auto", choices=["auto", "collide", "distance"],
@@ -487,6 +492,10 @@ def main():
                     help="bounding volumes of the static model B: 6 = AABB, 14/18/26-DOP (delta layout)")
     ap.add_argument("--layout", default="delta", choices=["delta", "fp16", "fp32"],
                     help="node box layout (fp16/fp32: the paper's half-vs-float ablation)")
+    ap.add_argument("--align-treelets", action="store_true",
+                    help="build aligned treelet blocks (staged in shared memory by default)")
+    ap.add_argument("--staging", default="auto", choices=["auto", "on", "off"],
+                    help="treelet staging in shared memory (auto: when the blobs are aligned)")
     ap.add_argument("--cpu-poses", type=int, default=100000)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-poses", type=int, default=2048, help="poses per --impl reference step")

@@ -196,6 +196,9 @@ typedef struct {
                      lower bound reaches the cap are pruned from the start (S:397-405 prune
                      rule with best initialised to c_i instead of +inf).  NaN caps act as
                      +inf, negative caps as 0.  Ignored by collide. */
+  int treelet_staging; /* 0 (auto): stage treelet blocks in shared memory when a blob has aligned treelets
+                          (cbvh_build_opts.align_treelets); 1: require it (CBVH_EINVAL otherwise); -1: never.
+                          AABB blobs only; results are identical either way. */
 } cbvh_query_opts;
 
 /* collide_batch / distance_batch with options (opts may be null). */
@@ -222,6 +225,9 @@ typedef struct {
   uint64_t timeline_ns[8];  /* when the pose cursor passed k/8 of N (ns after the kernel start) */
   uint64_t iterations;      /* warp expansion passes; bv_tests / (32 x iterations) = lane utilisation */
   uint64_t exact_tests;     /* triangle pairs past the leaf phase's cheap culls: exact Möller / distance evaluations */
+  uint64_t treelet_blocks;  /* treelet staging: blocks copied into shared memory */
+  uint64_t treelet_bytes;   /* treelet staging: their bytes (16-byte loads) */
+  uint64_t staged_reads;    /* treelet staging: child records decoded from shared memory */
 } cbvh_stats;
 
 /* Same as collide_batch / distance_batch but also accumulate cbvh_stats in

@@ -61,11 +61,13 @@ class cbvh_stats(C.Structure):
                 ("tri_tests", C.c_uint64), ("nodes_decoded", C.c_uint64), ("record_bytes", C.c_uint64),
                 ("tri_bytes", C.c_uint64), ("spills", C.c_uint64), ("kernel_ns", C.c_uint64),
                 ("tail_ns", C.c_uint64), ("dumped", C.c_uint64), ("timeline_ns", C.c_uint64 * 8),
-                ("iterations", C.c_uint64), ("exact_tests", C.c_uint64)]
+                ("iterations", C.c_uint64), ("exact_tests", C.c_uint64), ("treelet_blocks", C.c_uint64),
+                ("treelet_bytes", C.c_uint64), ("staged_reads", C.c_uint64)]
 
 
 class cbvh_query_opts(C.Structure):
-    _fields_ = [("descent", C.c_int), ("stats", C.c_int), ("early_exit", C.c_int), ("capped", C.c_int)]
+    _fields_ = [("descent", C.c_int), ("stats", C.c_int), ("early_exit", C.c_int), ("capped", C.c_int),
+                ("treelet_staging", C.c_int)]
 
 
 CBVH_DESCENT_SIMULTANEOUS, CBVH_DESCENT_LARGER = 0, 1

@@ -165,21 +165,30 @@ def validate_poses(poses, tol: float = 1e-6) -> np.ndarray:
     return np.nonzero(bad)[0]
 
 
-def _opts(descent: str, stats: bool, early_exit: bool = False, capped: bool = False) -> L.cbvh_query_opts:
+STAGING = {"auto": 0, "on": 1, "off": -1}
+
+
+def _opts(descent: str, stats: bool, early_exit: bool = False, capped: bool = False,
+          staging: str = "auto") -> L.cbvh_query_opts:
     if descent not in L.DESCENT:
         raise ValueError(f"descent must be one of {sorted(L.DESCENT)}")
-    return L.cbvh_query_opts(L.DESCENT[descent], 1 if stats else 0, 1 if early_exit else 0, 1 if capped else 0)
+    if staging not in STAGING:
+        raise ValueError(f"staging must be one of {sorted(STAGING)}")
+    return L.cbvh_query_opts(L.DESCENT[descent], 1 if stats else 0, 1 if early_exit else 0, 1 if capped else 0,
+                             STAGING[staging])
 
 
 def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=None,
                   workspace: Workspace | None = None, stream=None, stats: bool = False,
-                  descent: str = "larger", early_exit: bool = False):
+                  descent: str = "larger", early_exit: bool = False, staging: str = "auto"):
     """C-ABI collide_batch: per-pose hit flag (uint8) and colliding pair count (int32 view of uint32).
 
     descent: "larger" (default: descend the node with the larger box) or
     "simultaneous" (Alg. 1 verbatim).  Both give identical results.
     early_exit: stop each pose at its first hit (planning only needs the
     boolean); the hit flag is exact, the count a lower bound.
+    staging: treelet blocks staged in shared memory — "auto" (when a blob
+    was built with align_treelets), "on" (required) or "off".
 
     Device errors (a traversal-stack overflow) land in the workspace's error
     word: with a caller-supplied workspace, call ``check(workspace)`` after
@@ -200,7 +209,7 @@ def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=Non
         temp = workspace is None
         if temp:
             workspace = _temp_workspace(A, B, 0, dev, stream)
-        o = _opts(descent, stats, early_exit)
+        o = _opts(descent, stats, early_exit, staging=staging)
         L.check(L.load().collide_batch_ex(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
                                           C.c_void_p(hit.data_ptr()), C.c_void_p(count.data_ptr()),
                                           C.c_void_p(workspace.ptr), workspace.nbytes,
@@ -212,7 +221,7 @@ def collide_batch(A: CompressedBVH, B: CompressedBVH, poses, hit=None, count=Non
 
 def distance_batch(A: CompressedBVH, B: CompressedBVH, poses, dist=None,
                    workspace: Workspace | None = None, stream=None, stats: bool = False,
-                   descent: str = "larger", caps=None):
+                   descent: str = "larger", caps=None, staging: str = "auto"):
     """C-ABI distance_batch: per-pose minimum triangle–triangle distance (fp32).
     caps (optional, fp32 [N] on the poses' device): per-pose caps — the result
     is min(distance, cap), exact below the cap (cbvh_query_opts.capped).
@@ -234,7 +243,7 @@ def distance_batch(A: CompressedBVH, B: CompressedBVH, poses, dist=None,
         temp = workspace is None
         if temp:
             workspace = _temp_workspace(A, B, 1, dev, stream)
-        o = _opts(descent, stats, capped=caps is not None)
+        o = _opts(descent, stats, capped=caps is not None, staging=staging)
         L.check(L.load().distance_batch_ex(C.byref(A.bound), C.byref(B.bound), C.c_void_p(poses.data_ptr()), N,
                                            C.c_void_p(dist.data_ptr()), C.c_void_p(workspace.ptr), workspace.nbytes,
                                            C.c_void_p(_stream_ptr(stream)), C.byref(o)))

@@ -36,6 +36,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include <cfloat>
@@ -68,6 +69,8 @@ struct DevTree {
   uint32_t n_nodes, n_tris;  // bounds for the checked build
   uint32_t root_topo;
   int32_t root[6];   // decoded root lattice box
+  int tlog;          // aligned treelet blocks: log2 T (node id = block << tlog | offset); -1: not staged
+  int cb;            // code bytes per node (6 w / 8)
 };
 
 // k-DOP slab axes of the static model B beyond x, y, z (kdop/2 - 3 <= 10):
@@ -89,8 +92,11 @@ struct Control {
   unsigned long long t_frac[8];  // stats variant: when the pose cursor passed k/8 of N
   unsigned long long iterations; // stats variant: expansion passes (warp iterations)
   unsigned long long exact;      // stats variant: triangle pairs past the culls (exact Möller / distance)
+  unsigned long long stage_blocks, stage_bytes, stage_reads;  // stats variant: treelet blocks staged in smem,
+                                                              // their bytes, child records read from smem
 };
-static_assert(sizeof(Control) <= 256, "control block must fit the 256-byte workspace header");
+constexpr size_t kCtlBytes = 512;  // workspace header holding the control block
+static_assert(sizeof(Control) <= kCtlBytes, "control block must fit the workspace header");
 
 #ifndef CBVH_MIN_BLOCKS_DIST
 #define CBVH_MIN_BLOCKS_DIST 3
@@ -150,6 +156,8 @@ struct Params {
   int descent;           // CBVH_DESCENT_SIMULTANEOUS (Alg. 1 verbatim) or CBVH_DESCENT_LARGER
   int early_exit;        // collide: stop a pose's traversal at its first hit
   int capped;            // distance: dist holds per-pose caps on entry (cbvh_query_opts.capped)
+  int stage_slot_words;  // staging: words per smem slot (one treelet block: T topology words + T x cb code bytes)
+  int stage_sides;       // staging: bit 0 tree A, bit 1 tree B (CBVH_STAGE_SIDES, tuning; default both)
 };
 
 // item pose word: bits 0..29 pose id, bit 30 = descend a, bit 31 = descend b
@@ -1106,8 +1114,131 @@ struct WarpCtx {
   uint32_t* sq;     // exact-test queue SoA [3][kSurv]: pose, triangle of A, triangle of B
   uint32_t* scr;    // per-lane parking of the child boxes [12][32] (CBVH_SMEM_BOXES)
   uint32_t* spill;  // this warp's global spill area [kSpillCap][nfields(KX)]
+  uint32_t* stag;   // staging: slot tags [kStageSlots] (tree bit | block id; kNoBlock = empty)
+  uint32_t* stg;    // staging: slots [kStageSlots][stage_slot_words]
   int lane;
 };
+
+// ---------------------------------------------------------------- treelet staging
+// Treelet blocks in shared memory ("clustering BVHs into smaller
+// parts"; BJ north_star (2): "treelet blocks fetched with coalesced 16-byte
+// vector loads into shared memory").  With an aligned blob (align_treelets)
+// a T-slot block holds whole treelets and is one fixed-size span of the
+// topology and code arrays.  Each warp keeps kStageSlots blocks; every pass
+// the lanes that descend a side look their child's block up (one leader per
+// distinct block, __match_any_sync); a missing block is copied in by the
+// whole warp with 16-byte loads into the round-robin slot no lane of this
+// pass uses, and when every slot is taken the lane reads global memory as the
+// unstaged kernel does.  Children are then decoded from shared memory.
+#ifndef CBVH_STAGE_SLOTS
+#define CBVH_STAGE_SLOTS 4
+#endif
+static_assert(CBVH_STAGE_SLOTS >= 1 && CBVH_STAGE_SLOTS <= 8, "1..8 staging slots");
+constexpr int kStageSlots = CBVH_STAGE_SLOTS;
+constexpr int kStageTagWords = (kStageSlots + 3) & ~3;  // tags padded so the slots stay 16-byte aligned
+constexpr uint32_t kNoBlock = 0xFFFFFFFFu;
+constexpr uint32_t kTreeB = 0x40000000u;  // tag bit of tree B's blocks
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+
+// Look up (and, on a miss, copy in) the block of each lane's `node` of tree
+// T; returns the lane's slot or -1 (no node, or no free slot: read global).
+// All misses of the pass are copied together with asynchronous 16-byte
+// global->shared copies (cp.async, LDGSTS), so their latencies overlap.
+template <bool STATS>
+__device__ __forceinline__ int stage_block(const Params& p, const WarpCtx& c, const DevTree& T, uint32_t tree_bit,
+                                           uint32_t node, unsigned* used, unsigned* rr,
+                                           unsigned long long* s_blocks, unsigned long long* s_bytes) {
+  const uint32_t key = (node == kNoBlock || T.tlog < 0) ? kNoBlock : ((node >> T.tlog) | tree_bit);
+  if (!__any_sync(FULL, key != kNoBlock)) return -1;
+  const unsigned grp = __match_any_sync(FULL, key);
+  const int leader = __ffs(grp) - 1;
+  const bool lead = key != kNoBlock && c.lane == leader;
+  int s = -1;
+  if (lead) {
+    #pragma unroll
+    for (int q = 0; q < kStageSlots; ++q) s = c.stag[q] == key ? q : s;
+  }
+  *used |= __reduce_or_sync(FULL, (lead && s >= 0) ? (1u << s) : 0u);
+  unsigned miss = __ballot_sync(FULL, lead && s < 0);
+  if (miss) {
+    __syncwarp();  // every lane's reads of the previous pass are done before a slot is overwritten
+    // assign slots (round robin over the slots no lane of this pass uses)
+    unsigned long long fill = 0;  // bits 8k..8k+7: the slot of the k-th copied block
+    int nfill = 0;
+    unsigned m = miss;
+    while (m) {
+      const int l = __ffs(m) - 1;
+      m &= m - 1;
+      int v = -1;
+      #pragma unroll
+      for (int t = kStageSlots - 1; t >= 0; --t) {
+        const int q = (int)((*rr + (unsigned)t) % kStageSlots);
+        v = ((*used >> q) & 1u) ? v : q;
+      }
+      if (v < 0) break;  // every slot serves this pass: the rest read global memory
+      *rr = (unsigned)(v + 1) % kStageSlots;
+      *used |= 1u << v;
+      const uint32_t k = __shfl_sync(FULL, key, l);
+      if (c.lane == l) s = v;
+      if (c.lane == 0) c.stag[v] = k;
+      fill |= (unsigned long long)v << (8 * nfill);
+      ++nfill;
+    }
+    __syncwarp();  // the new tags are visible to every lane
+    // copy: nfill blocks x (nt + nc) 16-byte chunks, spread over the lanes
+    const int nt = (1 << T.tlog) >> 2, nc = ((1 << T.tlog) * T.cb) >> 4, per = nt + nc;
+    for (int q = c.lane; q < nfill * per; q += 32) {
+      const int b = q / per, r = q - b * per;
+      const int v = (int)((fill >> (8 * b)) & 255u);
+      const size_t first = (size_t)(c.stag[v] & ~kTreeB) << T.tlog;
+      const void* src = r < nt ? static_cast<const void*>(T.topo + first + 4 * r)
+                               : static_cast<const void*>(T.codes + first * T.cb + 16 * (r - nt));
+      cp_async16(c.stg + v * p.stage_slot_words + 4 * r, src);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    if (STATS && c.lane == 0) { *s_blocks += nfill; *s_bytes += 16ull * per * nfill; }
+  }
+  __syncwarp();
+  s = __shfl_sync(FULL, s, leader);
+  return key == kNoBlock ? -1 : s;
+}
+
+// The codes of a node record at `rec` (global or shared memory), fields as load_codes
+__device__ __forceinline__ void load_codes_at(const uint8_t* rec, int width, uint32_t q[6]) {
+  if (width == 8) {
+    const unsigned short* r = reinterpret_cast<const unsigned short*>(rec);
+    const uint32_t a = r[0], b = r[1], c = r[2];
+    q[0] = a & 255u; q[1] = a >> 8; q[2] = b & 255u; q[3] = b >> 8; q[4] = c & 255u; q[5] = c >> 8;
+  } else if (width == 16) {
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(rec);
+    const uint32_t a = r[0], b = r[1], c = r[2];
+    q[0] = a & 0xffffu; q[1] = a >> 16; q[2] = b & 0xffffu; q[3] = b >> 16; q[4] = c & 0xffffu; q[5] = c >> 16;
+  } else {
+    const uint32_t w = (uint32_t)rec[0] | ((uint32_t)rec[1] << 8) | ((uint32_t)rec[2] << 16);
+    #pragma unroll
+    for (int f = 0; f < 6; ++f) q[f] = (w >> (4 * f)) & 15u;
+  }
+}
+
+// A child's topology word and decoded box: from its staged block (slot >= 0)
+// or from global memory.
+__device__ __forceinline__ uint32_t fetch_child(const WarpCtx& c, const Params& p, const DevTree& T, int slot,
+                                                uint32_t node, const int32_t P[6], int32_t C[6]) {
+  if (slot >= 0) {
+    const uint32_t* blk = c.stg + slot * p.stage_slot_words;
+    const uint32_t loc = node & ((1u << T.tlog) - 1u);
+    uint32_t q[6];
+    load_codes_at(reinterpret_cast<const uint8_t*>(blk + (1 << T.tlog)) + loc * T.cb, T.width, q);
+    decode_child(P, q, T.bits, C);
+    return blk[loc];
+  }
+  fetch_child_box(T, node, P, C);
+  return __ldg(T.topo + node);
+}
 
 // Drain the leaf queue: checkPrimitives over every queued leaf pair,
 // the c_A x c_B triangle pairs spread over the 32 lanes.  Returns the number
@@ -1399,7 +1530,7 @@ __host__ __device__ constexpr int min_blocks(int mode, int kx) {
   return kx == 0 ? (mode == 0 ? CBVH_MIN_BLOCKS : CBVH_MIN_BLOCKS_DIST) : (mode == 0 ? (kx >= 10 ? 3 : 4) : 3);
 }
 
-template <int MODE, bool STATS, int KX>
+template <int MODE, bool STATS, int KX, bool STAGE>
 __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_kernel(const __grid_constant__ Params p) {
   constexpr int NF = nfields(KX);
   extern __shared__ uint32_t smem[];
@@ -1411,6 +1542,15 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
   c.sq = c.lq + 5 * kLeafQ;
   c.scr = c.sq + (MODE == 1 ? 3 * kSurv : 0);
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * NF;
+  // staging area after all warps' stacks and queues
+  c.stag = smem + kWarps * warp_smem_words(MODE, KX) + wib * (kStageTagWords + kStageSlots * p.stage_slot_words);
+  c.stg = c.stag + kStageTagWords;
+  unsigned st_used = 0, st_rr = 0;
+  unsigned long long s_sblk = 0, s_sbytes = 0, s_sreads = 0;
+  if (STAGE) {
+    if (c.lane < kStageSlots) c.stag[c.lane] = kNoBlock;
+    __syncwarp();
+  }
   int top = 0, nleaf = 0, spill_top = 0;
   int after = 0;  // iterations since the input ran out (before that: the poll counter)
   unsigned long long s_dump = 0, s_iter = 0, s_exact = 0;
@@ -1643,6 +1783,19 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       const float eps = 2e-6f * (tmax + scale_ab);
       int32_t BA[6], BB[6], BX[2 * KX + 1];
 #endif
+      // treelet staging: the blocks of this pass's children, warp-wide
+      int slotA = -1, slotB = -1;
+      if (STAGE) {
+        st_used = 0;
+        uint32_t na = kNoBlock, nbn = kNoBlock;
+        if (valid && a_int) na = (ta & 0x0FFFFFFFu) + (uint32_t)i;
+        if (valid && b_int) nbn = (tb & 0x0FFFFFFFu) + (uint32_t)j;
+        if (na != kNoBlock && na >= p.A.n_nodes) na = kNoBlock;
+        if (nbn != kNoBlock && nbn >= p.B.n_nodes) nbn = kNoBlock;
+        if (p.stage_sides & 1) slotA = stage_block<STATS>(p, c, p.A, 0u, na, &st_used, &st_rr, &s_sblk, &s_sbytes);
+        if (p.stage_sides & 2) slotB = stage_block<STATS>(p, c, p.B, kTreeB, nbn, &st_used, &st_rr, &s_sblk, &s_sbytes);
+        if (STATS) s_sreads += (slotA >= 0 ? 1 : 0) + (slotB >= 0 ? 1 : 0);
+      }
       if (valid) {
 #if CBVH_LATE_LOADS
         #pragma unroll
@@ -1656,8 +1809,11 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
         if (a_int) {
           uint32_t node = (ta & 0x0FFFFFFFu) + (uint32_t)i;
           CBVH_GUARD(p, node < p.A.n_nodes, (node = 0, bad = true));
-          cta = __ldg(p.A.topo + node);
-          fetch_child_box(p.A, node, BA, CA);
+          if (STAGE) cta = fetch_child(c, p, p.A, slotA, node, BA, CA);
+          else {
+            cta = __ldg(p.A.topo + node);
+            fetch_child_box(p.A, node, BA, CA);
+          }
         } else {
           #pragma unroll
           for (int r = 0; r < 6; ++r) CA[r] = BA[r];
@@ -1665,9 +1821,15 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
         if (b_int) {
           uint32_t node = (tb & 0x0FFFFFFFu) + (uint32_t)j;
           CBVH_GUARD(p, node < p.B.n_nodes, (node = 0, bad = true));
-          ctb = __ldg(p.B.topo + node);
-          if constexpr (KX > 0) fetch_child_kdop<KX>(p.B, node, BB, BX, CB, CX);
-          else fetch_child_box(p.B, node, BB, CB);
+          if constexpr (KX > 0) {
+            ctb = __ldg(p.B.topo + node);
+            fetch_child_kdop<KX>(p.B, node, BB, BX, CB, CX);
+          } else if (STAGE) {
+            ctb = fetch_child(c, p, p.B, slotB, node, BB, CB);
+          } else {
+            ctb = __ldg(p.B.topo + node);
+            fetch_child_box(p.B, node, BB, CB);
+          }
         } else {
           #pragma unroll
           for (int r = 0; r < 6; ++r) CB[r] = BB[r];
@@ -1885,6 +2047,16 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       atomicAdd(&p.ctl->iterations, s_iter);
       atomicAdd(&p.ctl->exact, ex);
     }
+    if (STAGE) {
+      unsigned long long sr = s_sreads;
+      #pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sr += __shfl_down_sync(FULL, sr, o);
+      if (c.lane == 0) {
+        atomicAdd(&p.ctl->stage_blocks, s_sblk);
+        atomicAdd(&p.ctl->stage_bytes, s_sbytes);
+        atomicAdd(&p.ctl->stage_reads, sr);
+      }
+    }
   }
 }
 
@@ -1917,6 +2089,7 @@ __global__ void init_kernel(Params p, int reset_stats) {
       p.ctl->dumped = 0ull;
       p.ctl->iterations = 0ull;
       p.ctl->exact = 0ull;
+      p.ctl->stage_blocks = p.ctl->stage_bytes = p.ctl->stage_reads = 0ull;
       for (int s = 0; s < 8; ++s) p.ctl->t_frac[s] = ~0ull;
     }
   }
@@ -1949,27 +2122,34 @@ struct LaunchShape {
 
 constexpr int kMaxDevices = 64;
 
-template <int MODE, bool STATS, int KX>
-static int shape_for(LaunchShape* s) {
+// Grid of the persistent traversal kernel: SMs x resident CTAs at `smem`
+// bytes of dynamic shared memory per CTA.
+template <int MODE, bool STATS, int KX, bool STAGE>
+static int shape_for(LaunchShape* s, size_t smem) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
   // the dynamic shared-memory opt-in and the occupancy are per device: cached
-  // per device (a race only repeats the idempotent calls)
+  // per device (a race only repeats the idempotent calls); the staged kernel's
+  // shared memory depends on the blobs, so its occupancy is queried per call
   static std::atomic<int> cached[kMaxDevices];
   const int slot = dev < kMaxDevices ? dev : -1;
-  per_sm = slot >= 0 ? cached[slot].load(std::memory_order_acquire) : 0;
+  per_sm = (slot >= 0 && !STAGE) ? cached[slot].load(std::memory_order_acquire) : 0;
   if (per_sm == 0) {
-    e = cudaFuncSetAttribute(traverse_kernel<MODE, STATS, KX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_bytes(MODE, KX));
+    int optin = 0;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    if (smem > (size_t)optin) return set_error(CBVH_EINVAL, "shared memory of the staged kernel exceeds the device limit");
+    e = cudaFuncSetAttribute(traverse_kernel<MODE, STATS, KX, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             STAGE ? optin : (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel<MODE, STATS, KX>, kWarps * 32,
-                                                      smem_bytes(MODE, KX));
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel<MODE, STATS, KX, STAGE>, kWarps * 32,
+                                                      smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
-    if (slot >= 0) cached[slot].store(per_sm, std::memory_order_release);
+    if (slot >= 0 && !STAGE) cached[slot].store(per_sm, std::memory_order_release);
   }
   s->blocks = sms * per_sm;
   s->warps = s->blocks * kWarps;
@@ -1980,9 +2160,11 @@ template <int KX>
 static int max_warps_kx(int mode) {
   // workspace is sized for the larger of the instantiations of this mode
   LaunchShape a{}, b{};
-  int rc = mode == 0 ? shape_for<0, false, KX>(&a) : shape_for<1, false, KX>(&a);
+  // (the staged kernel uses more shared memory, so never more warps)
+  int rc = mode == 0 ? shape_for<0, false, KX, false>(&a, smem_bytes(0, KX))
+                     : shape_for<1, false, KX, false>(&a, smem_bytes(1, KX));
   if (rc) return -1;
-  rc = mode == 0 ? shape_for<0, true, KX>(&b) : shape_for<1, true, KX>(&b);
+  rc = mode == 0 ? shape_for<0, true, KX, false>(&b, smem_bytes(0, KX)) : shape_for<1, true, KX, false>(&b, smem_bytes(1, KX));
   if (rc) return -1;
   return a.warps > b.warps ? a.warps : b.warps;
 }
@@ -1998,7 +2180,7 @@ static int max_warps(int mode, int kx) {
 }
 
 static size_t workspace_for_warps(int warps, int kx) {
-  return 256 + (size_t)warps * kSpillCap * nfields(kx) * sizeof(uint32_t) +
+  return kCtlBytes + (size_t)warps * kSpillCap * nfields(kx) * sizeof(uint32_t) +
          2 * (size_t)kContCap * nfields(kx) * sizeof(uint32_t);
 }
 
@@ -2057,13 +2239,19 @@ static DevTree make_tree(const cbvh_bvh* T) {
   d.layout = (int)h.layout;
   d.n_nodes = h.num_nodes;
   d.n_tris = h.num_tris;
+  d.cb = (int)(h.kdop * h.code_width / 8);
+  d.tlog = -1;
+  const uint32_t Tn = h.treelet_nodes;
+  if ((h.flags & CBVH_FLAG_ALIGNED_TREELETS) && h.kdop == 6 && Tn >= 4 && (Tn & (Tn - 1)) == 0 &&
+      (Tn * (uint32_t)d.cb) % 16 == 0)
+    for (d.tlog = 0; (1u << d.tlog) < Tn; ++d.tlog) {}
   return d;
 }
 
 template <int MODE, bool STATS, int KX>
 static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                      uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream, int descent,
-                     int early_exit, int capped) {
+                     int early_exit, int capped, int stage) {
   g_launches = 0;
   if (!A || !B || !d_ws) return set_error(CBVH_EINVAL, "null argument");
   if (N < 0 || N > 0x3fffffffLL) return set_error(CBVH_EINVAL, "N out of range [0, 2^30)");
@@ -2075,14 +2263,29 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   if (!A->d_blob || !B->d_blob) return set_error(CBVH_EINVAL, "unbound bvh");
   if ((reinterpret_cast<uintptr_t>(d_poses) & 15) != 0) return set_error(CBVH_EINVAL, "poses must be 16-byte aligned");
   if ((reinterpret_cast<uintptr_t>(d_ws) & 255) != 0) return set_error(CBVH_EINVAL, "workspace must be 256-byte aligned");
-  LaunchShape s;
-  int rc = shape_for<MODE, STATS, KX>(&s);
-  if (rc) return rc;
-  if (ws_bytes < workspace_for_warps(s.warps, KX)) return set_error(CBVH_EWORKSPACE, "workspace too small");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   Params p;
   p.A = make_tree(A);
   p.B = make_tree(B);
+  // treelet staging (KX = 0 only): the slot holds the larger of the two
+  // trees' blocks; a tree whose blob is not aligned is read from global memory
+  if (KX != 0 || (p.A.tlog < 0 && p.B.tlog < 0)) stage = 0;
+  p.stage_slot_words = 0;
+  static const int sides = [] {
+    const char* env = std::getenv("CBVH_STAGE_SIDES");
+    return (env && *env) ? std::atoi(env) : 3;
+  }();
+  p.stage_sides = sides;
+  for (const DevTree* T : {&p.A, &p.B})
+    if (stage && T->tlog >= 0) p.stage_slot_words = std::max(p.stage_slot_words, ((1 << T->tlog) * (4 + T->cb)) / 4);
+  const size_t smem = smem_bytes(MODE, KX) +
+                      (stage ? (size_t)kWarps * (kStageTagWords + kStageSlots * p.stage_slot_words) * sizeof(uint32_t) : 0);
+  LaunchShape s;
+  int rc;
+  if constexpr (KX == 0) rc = stage ? shape_for<MODE, STATS, KX, true>(&s, smem) : shape_for<MODE, STATS, KX, false>(&s, smem);
+  else rc = shape_for<MODE, STATS, KX, false>(&s, smem);
+  if (rc) return rc;
+  if (ws_bytes < workspace_for_warps(s.warps, KX)) return set_error(CBVH_EWORKSPACE, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
   std::memcpy(p.A.root, A->root_decoded, sizeof p.A.root);
   std::memcpy(p.B.root, B->root_decoded, sizeof p.B.root);
   p.A.root_topo = A->root_topo;
@@ -2102,7 +2305,7 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   p.count = d_count;
   p.dist_bits = reinterpret_cast<uint32_t*>(d_dist);
   p.ctl = static_cast<Control*>(d_ws);
-  p.spill = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + 256);
+  p.spill = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) + kCtlBytes);
   uint32_t* cont0 = p.spill + (size_t)s.warps * kSpillCap * nfields(KX);
   uint32_t* cont1 = cont0 + (size_t)kContCap * nfields(KX);
   p.descent = descent;
@@ -2134,7 +2337,12 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
     p.budget = ph < nb ? budgets[ph] : -1;
     p.cont_in = (ph & 1) ? cont0 : cont1;   // phase ph reads what ph - 1 wrote
     p.cont_out = (ph & 1) ? cont1 : cont0;
-    traverse_kernel<MODE, STATS, KX><<<s.blocks, kWarps * 32, smem_bytes(MODE, KX), st>>>(p);
+    if constexpr (KX == 0) {
+      if (stage) traverse_kernel<MODE, STATS, KX, true><<<s.blocks, kWarps * 32, smem, st>>>(p);
+      else traverse_kernel<MODE, STATS, KX, false><<<s.blocks, kWarps * 32, smem, st>>>(p);
+    } else {
+      traverse_kernel<MODE, STATS, KX, false><<<s.blocks, kWarps * 32, smem, st>>>(p);
+    }
     g_launches++;
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "traverse_kernel launch");
@@ -2148,15 +2356,20 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
 template <int MODE, bool STATS>
 static int launch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                   uint32_t* d_count, float* d_dist, void* d_ws, size_t ws_bytes, void* stream, int descent,
-                  int early_exit, int capped) {
+                  int early_exit, int capped, int stage) {
   g_launches = 0;
   if (!A || !B) return set_error(CBVH_EINVAL, "null argument");
   if (A->h.kdop != 6) return set_error(CBVH_EINVAL, "k-DOP blobs bound the static model B only; A must be an AABB blob");
+  // treelet staging: auto (0) = on when a blob has aligned treelet blocks
+  const bool aligned = ((A->h.flags | B->h.flags) & CBVH_FLAG_ALIGNED_TREELETS) != 0;
+  if (stage > 0 && (!aligned || extra_axes(B) != 0))
+    return set_error(CBVH_EINVAL, "treelet staging needs an aligned-treelet blob (align_treelets) and AABBs");
+  const int st = stage < 0 ? 0 : (aligned ? 1 : 0);
   switch (extra_axes(B)) {
-    case 0: return launch_kx<MODE, STATS, 0>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped);
-    case 4: return launch_kx<MODE, STATS, 4>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped);
-    case 6: return launch_kx<MODE, STATS, 6>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped);
-    case 10: return launch_kx<MODE, STATS, 10>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped);
+    case 0: return launch_kx<MODE, STATS, 0>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped, st);
+    case 4: return launch_kx<MODE, STATS, 4>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped, 0);
+    case 6: return launch_kx<MODE, STATS, 6>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped, 0);
+    case 10: return launch_kx<MODE, STATS, 10>(A, B, d_poses, N, d_hit, d_count, d_dist, d_ws, ws_bytes, stream, descent, early_exit, capped, 0);
   }
   return set_error(CBVH_EINVAL, "bad k-DOP");
 }
@@ -2292,18 +2505,19 @@ static int opts_descent(const cbvh_query_opts* o) { return o ? o->descent : CBVH
 static int opts_early(const cbvh_query_opts* o) { return o ? o->early_exit : 0; }
 static int opts_capped(const cbvh_query_opts* o) { return o ? o->capped : 0; }
 static int opts_stats(const cbvh_query_opts* o) { return o ? o->stats : 0; }
+static int opts_stage(const cbvh_query_opts* o) { return o ? o->treelet_staging : 0; }
 
 int collide_batch_ex(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                      uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream, const cbvh_query_opts* o) {
   if (opts_stats(o))
-    return launch<0, true>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o));
-  return launch<0, false>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o));
+    return launch<0, true>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o), opts_stage(o));
+  return launch<0, false>(A, B, d_poses, N, d_hit, d_pair_count, nullptr, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o), opts_stage(o));
 }
 int distance_batch_ex(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, float* d_min_dist,
                       void* d_ws, size_t ws_bytes, void* stream, const cbvh_query_opts* o) {
   if (opts_stats(o))
-    return launch<1, true>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o));
-  return launch<1, false>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o));
+    return launch<1, true>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o), opts_stage(o));
+  return launch<1, false>(A, B, d_poses, N, nullptr, nullptr, d_min_dist, d_ws, ws_bytes, stream, opts_descent(o), opts_early(o), opts_capped(o), opts_stage(o));
 }
 int collide_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                   uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream) {
@@ -2311,7 +2525,7 @@ int collide_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, in
 }
 int collide_batch_stats(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, uint8_t* d_hit,
                         uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream) {
-  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1, 0, 0};
+  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1, 0, 0, 0};
   return collide_batch_ex(A, B, d_poses, N, d_hit, d_pair_count, d_ws, ws_bytes, stream, &o);
 }
 int distance_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N, float* d_min_dist,
@@ -2320,7 +2534,7 @@ int distance_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, i
 }
 int distance_batch_stats(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N,
                          float* d_min_dist, void* d_ws, size_t ws_bytes, void* stream) {
-  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1, 0, 0};
+  cbvh_query_opts o{CBVH_DESCENT_LARGER, 1, 0, 0, 0};
   return distance_batch_ex(A, B, d_poses, N, d_min_dist, d_ws, ws_bytes, stream, &o);
 }
 
@@ -2351,6 +2565,9 @@ int cbvh_read_stats(const void* d_ws, cbvh_stats* out, void* stream) {
   out->dumped = ctl.dumped;
   out->iterations = ctl.iterations;
   out->exact_tests = ctl.exact;
+  out->treelet_blocks = ctl.stage_blocks;
+  out->treelet_bytes = ctl.stage_bytes;
+  out->staged_reads = ctl.stage_reads;
   for (int k = 0; k < 8; ++k)
     out->timeline_ns[k] = (timed && ctl.t_frac[k] != ~0ull && ctl.t_frac[k] >= ctl.t_start) ? ctl.t_frac[k] - ctl.t_start : 0;
   return CBVH_OK;

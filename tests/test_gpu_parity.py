@@ -53,9 +53,17 @@ def run_distance(M, A, B, poses, stats=False, descent="larger"):
     return out
 
 
-def build(M, mesh, B, bits, T=32, layout="delta", kdop=6):
+def build(M, mesh, B, bits, T=32, layout="delta", kdop=6, aligned=False):
     return M.build_compressed_bvh(mesh.vertices, mesh.triangles, B, bits, T, 4, layout=layout,
-                                  kdop=kdop).to_device()
+                                  kdop=kdop, align_treelets=aligned).to_device()
+
+
+def run_collide_staged(M, A, B, poses, staging):
+    P = torch.from_numpy(np.ascontiguousarray(poses)).cuda()
+    ws = M.Workspace(A, B, 0)
+    hit, cnt = M.collide_batch(A, B, P, workspace=ws, stats=True, staging=staging)
+    M.check(ws)
+    return hit.cpu().numpy(), cnt.cpu().numpy().view(np.uint32).astype(np.int64), M.read_stats(ws)
 
 
 def oracle_trees(w):
@@ -230,6 +238,53 @@ def test_contact_preset_collide_and_distance(M):
     drep = check_distance(d, d64, delta, "contact distance")
     assert np.median(d64[d64 > 0]) < 0.05
     print("contact", rep, drep)
+
+
+@pytest.mark.parametrize("Bf,bits,T", [(2, 8, 32), (4, 8, 32), (4, 8, 64), (8, 16, 64), (4, 4, 16)])
+def test_config1_treelet_staging(M, cfg1, Bf, bits, T):
+    # treelet blocks staged in shared memory (align_treelets):
+    # band rule vs the oracle, counts identical to the unstaged kernel on the
+    # same blobs and on packed (unaligned) blobs, and blocks really staged
+    w, tA, tB, delta, cnt, H, Z = cfg1
+    A, B = build(M, w.A, Bf, bits, T, aligned=True), build(M, w.B, Bf, bits, T, aligned=True)
+    hit, gc, st = run_collide_staged(M, A, B, w.poses, "on")
+    check_collide(hit, gc, H, Z, f"staged B={Bf} b={bits} T={T}")
+    h0, c0, st0 = run_collide_staged(M, A, B, w.poses, "off")
+    assert np.array_equal(gc, c0) and np.array_equal(hit, h0)
+    hp, cp, _ = run_collide_staged(M, build(M, w.A, Bf, bits, T), build(M, w.B, Bf, bits, T), w.poses, "auto")
+    assert np.array_equal(gc, cp)
+    assert st["treelet_blocks"] > 0 and st["staged_reads"] > 0 and st0["treelet_blocks"] == 0
+    assert st["bv_tests"] == st0["bv_tests"]
+    # the staged reads plus the (all-slots-busy) global fallbacks are every decoded child
+    assert st["staged_reads"] <= st["nodes_decoded"]
+    # only one side aligned: that side is staged, the other read from global memory
+    _, c1, s1 = run_collide_staged(M, A, build(M, w.B, Bf, bits, T), w.poses, "on")
+    assert np.array_equal(c1, gc) and s1["treelet_blocks"] > 0
+    P = torch.from_numpy(w.poses[:256]).cuda()
+    d = M.distance_batch(A, B, P, staging="on").cpu().numpy()
+    d64, _ = O.distance(tA, tB, w.poses[:256])
+    check_distance(d, d64, delta, f"staged distance B={Bf}")
+    with pytest.raises(M._lib.CbvhError, match="EINVAL"):
+        M.collide_batch(build(M, w.A, Bf, bits, T), build(M, w.B, Bf, bits, T), P, staging="on")
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_zero_separation_preset(M, k):
+    # the paper's "distance of zero" preset by bisection with the
+    # oracle: every pose's oracle distance is in (0, 1e-3);
+    # collide (band rule) and distance (1e-5 relative) through the C-ABI
+    n = 1024 if k == 1 else 2048
+    w = G.make_config(k, num_poses=n, preset="zero")
+    tA, tB = oracle_trees(w)
+    delta = O.band_delta(w.A.vertices)
+    d64, _ = O.distance(tA, tB, w.poses)
+    assert np.all((d64 > 0) & (d64 < 1e-3))
+    _, H, Z, _ = O.collide(tA, tB, w.poses, delta)
+    A, B = build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet)
+    hit, gc = run_collide(M, A, B, w.poses)
+    rep = check_collide(hit, gc, H, Z, f"zero cfg{k}")
+    drep = check_distance(run_distance(M, A, B, w.poses), d64, delta, f"zero cfg{k} distance")
+    print("zero preset", k, rep, drep)
 
 
 # ------------------------------------------------------------------ tiny + degenerate
@@ -457,6 +512,19 @@ def test_config5_kdop_full_size(M):
         hit, gc = run_collide(M, A, build(M, w.B, w.branching, w.bits, w.treelet, kdop=k), w.poses)
         assert np.array_equal(gc, ref), k
         check_collide(hit[idx], gc[idx], H, Z, f"cfg5 k={k}")
+
+
+def test_config5_treelet_staging_full_size(M):
+    # full config 5 batch on aligned blobs (T = 64): the staged kernel counts
+    # exactly what the unstaged kernel counts on every pose
+    w = G.make_config(5)
+    A = build(M, w.A, w.branching, w.bits, w.treelet, aligned=True)
+    B = build(M, w.B, w.branching, w.bits, w.treelet, aligned=True)
+    h1, c1, s1 = run_collide_staged(M, A, B, w.poses, "on")
+    h0, c0, s0 = run_collide_staged(M, A, B, w.poses, "off")
+    assert np.array_equal(c1, c0) and np.array_equal(h1, h0)
+    assert s1["treelet_blocks"] > 0 and s1["bv_tests"] == s0["bv_tests"]
+    print("cfg5 staging", {k: s1[k] for k in ("treelet_blocks", "treelet_bytes", "staged_reads", "nodes_decoded")})
 
 
 def test_config5_early_exit_full_size(M):
