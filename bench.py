@@ -274,9 +274,9 @@ def run(args):
     if args.bits:
         w.bits = args.bits
     A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout,
-                               align_treelets=args.align_treelets)
+                               align_treelets=args.align_treelets, zero_suppress=args.zero_suppress)
     B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout,
-                               kdop=args.kdop, align_treelets=args.align_treelets)
+                               kdop=args.kdop, align_treelets=args.align_treelets, zero_suppress=args.zero_suppress)
     distance = (w.mode if args.mode == "auto" else args.mode) == "distance"
     build_s = time.time() - t0
     A.to_device(dev)
@@ -354,7 +354,8 @@ def run(args):
                               "treelet_blocks": st["treelet_blocks"], "staged_reads": st["staged_reads"],
                               "nodes_decoded": st["nodes_decoded"],
                               "iterations": st["iterations"], "bv_tests": st["bv_tests"], "leaf_pairs": st["leaf_pairs"], "tri_tests": st["tri_tests"], "exact_tests": st["exact_tests"], "layout": args.layout, "kdop": args.kdop, "early_exit": args.early_exit,
-                              "bytes_per_node": {"A": A.info["bytes_per_node"], "B": B.info["bytes_per_node"]}}), flush=True)
+                              "bytes_per_node": {"A": A.info["bytes_per_node"], "B": B.info["bytes_per_node"]},
+                              "bvh_bytes": {"A": A.info["bvh_bytes"], "B": B.info["bvh_bytes"]}}), flush=True)
         return
 
     # ---- stats run (untimed): BV-pair tests and algorithmic bytes per launch
@@ -422,7 +423,8 @@ def run(args):
                        "descent": args.descent + (" (one side per internal pair, DESIGN R15)" if args.descent == "larger"
                                                   else " (Alg. 1 verbatim)"),
                        "early_exit": bool(args.early_exit), "preset": args.preset,
-                       "align_treelets": bool(args.align_treelets), "staging": args.staging,
+                       "align_treelets": bool(args.align_treelets), "zero_suppress": bool(args.zero_suppress),
+                       "staging": args.staging,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"pose-sharded x{world} (independent batches)"},
             "bv_pair_tests_per_s": st["bv_tests"] / (statistics.median(step_ms) / 1e3),
@@ -494,6 +496,8 @@ def main():
                     help="node box layout (fp16/fp32: the paper's half-vs-float ablation)")
     ap.add_argument("--align-treelets", action="store_true",
                     help="build aligned treelet blocks (staged in shared memory by default)")
+    ap.add_argument("--zero-suppress", action="store_true",
+                    help="integer-compressed corrections (presence masks; implies aligned treelet blocks)")
     ap.add_argument("--staging", default="auto", choices=["auto", "on", "off"],
                     help="treelet staging in shared memory (auto: when the blobs are aligned)")
     ap.add_argument("--cpu-poses", type=int, default=100000)

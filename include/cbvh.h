@@ -74,6 +74,10 @@ typedef struct {
                         is one aligned, fixed-size span of the topology and code arrays that the traversal
                         can stage in shared memory.  Needs the delta AABB layout and a
                         power-of-two T in [4, 64] */
+  int zero_suppress;  /* non-zero: integer-compressed corrections ("compress it using integer compression
+                        method"): per treelet block, a presence mask per node and only its non-zero fields
+                        (implies align_treelets; delta AABB layout, bits > 4).  Decoded from the staged
+                        block, so queries on such blobs stage treelets */
 } cbvh_build_opts;
 
 /* Build the compressed BVH of one mesh ("splitting the models and wrap it
@@ -107,10 +111,11 @@ typedef struct {
   uint64_t off_axes;   /* k-DOP axis table: per extra axis {fp32 origin, int32 exp, int32 root lo, root hi} */
   uint32_t flags;      /* CBVH_FLAG_* */
   uint32_t real_nodes; /* nodes of the tree (num_nodes counts node slots, padding included) */
+  uint64_t off_blocks; /* zero-suppressed codes: per-block region offsets (u32, 16-byte units from off_codes) */
 } cbvh_header;
 
 /* cbvh_header.flags */
-enum { CBVH_FLAG_ALIGNED_TREELETS = 1 };
+enum { CBVH_FLAG_ALIGNED_TREELETS = 1, CBVH_FLAG_ZERO_SUPPRESSED = 2 };
 
 typedef struct {
   cbvh_header h;

@@ -406,10 +406,12 @@ struct BlobView {
   uint32_t layout;  // 0 delta (lattice corrections), 1 absolute binary16, 2 absolute fp32
   uint32_t kdop;    // 6 (AABB) or 14 / 18 / 26: k/2 slab axes per node
   uint64_t off_axes;
-  uint32_t flags;       // bit 0: aligned treelets — treelet k owns node slots [k T, k T + T)
+  uint32_t flags;       // bit 0: aligned treelet blocks of T slots; bit 1: zero-suppressed codes
   uint32_t real_nodes;  // nodes of the tree; n_nodes counts slots (padding included)
+  uint64_t off_blocks;  // zero-suppressed: per-block region offsets (u32, 16-byte units from off_codes)
   uint32_t nax() const { return kdop / 2; }
   bool aligned() const { return flags & 1u; }
+  bool zero_suppressed() const { return flags & 2u; }
 };
 
 // Topology word of an unused (padding) slot of an aligned treelet.
@@ -433,7 +435,9 @@ bool parse_blob(const uint8_t* p, size_t bytes, BlobView* b) {
   b->off_axes = rd<uint64_t>(p, 144);
   b->flags = rd<uint32_t>(p, 152);
   b->real_nodes = rd<uint32_t>(p, 156);
-  if (b->flags > 1u || b->real_nodes == 0 || b->real_nodes > b->n_nodes) return false;
+  b->off_blocks = rd<uint64_t>(p, 160);
+  if (b->flags > 3u || b->real_nodes == 0 || b->real_nodes > b->n_nodes) return false;
+  if (b->zero_suppressed() && (!b->aligned() || b->w < 8 || b->layout != 0 || b->kdop != 6)) return false;
   if (!b->aligned() && b->real_nodes != b->n_nodes) return false;
   if (b->aligned() && b->n_nodes % b->T != 0) return false;
   if (b->kdop != 6 && b->kdop != 14 && b->kdop != 18 && b->kdop != 26) return false;
@@ -475,6 +479,21 @@ uint32_t blob_topo(const BlobView& b, uint32_t n) { return rd<uint32_t>(b.p, b.o
 // axes; axes 0-2 are x, y, z): w-bit unsigned, little-endian, 4-bit fields
 // packed two per byte (low nibble first).
 uint32_t code_field(const BlobView& b, uint32_t n, uint32_t f) {
+  if (b.zero_suppressed()) {
+    // block n / T holds, from off_codes + 16 * table[block]: T presence masks
+    // (bit f set = field f stored), then the stored fields of its nodes in
+    // node order, w/8 bytes each, little-endian; absent fields are zero
+    const uint32_t blk = n / b.T, j = n % b.T;
+    const uint64_t region = b.off_codes + 16ull * rd<uint32_t>(b.p, b.off_blocks + 4ull * blk);
+    const uint32_t m = b.p[region + j];
+    if (!((m >> f) & 1u)) return 0;
+    uint64_t k = 0;  // fields stored before this one
+    for (uint32_t i = 0; i < j; ++i)
+      for (int g = 0; g < 6; ++g) k += (b.p[region + i] >> g) & 1u;
+    for (uint32_t g = 0; g < f; ++g) k += (m >> g) & 1u;
+    const uint64_t at = region + b.T + k * (b.w / 8);
+    return b.w == 16 ? (uint32_t)rd<uint16_t>(b.p, at) : (uint32_t)b.p[at];
+  }
   const uint64_t base = b.off_codes + (uint64_t)n * (2ull * b.nax() * b.w / 8);
   if (b.w == 16) return rd<uint16_t>(b.p, base + 2 * f);
   if (b.w == 8) return b.p[base + f];
@@ -1025,8 +1044,27 @@ int64_t oracle_check_blob(const uint8_t* blob, uint64_t bytes, const float* vert
     if (seen[n]) { ++reached; continue; }
     if (!b.aligned() || blob_topo(b, n) != kPadSlot) { report[0]++; continue; }
     for (uint32_t f = 0; f < 2 * b.nax(); ++f) if (code_field(b, n, f) != 0) report[0]++;
+    if (b.zero_suppressed() &&
+        b.p[b.off_codes + 16ull * rd<uint32_t>(b.p, b.off_blocks + 4ull * (n / b.T)) + n % b.T] != 0)
+      report[0]++;
   }
   if (reached != b.real_nodes) report[0]++;
+  if (b.zero_suppressed()) {
+    // regions in block order, inside [off_codes, off_blocks), each large
+    // enough for its masks and the fields they announce; masks use 6 bits
+    const uint64_t nblocks = b.n_nodes / b.T;
+    for (uint64_t k = 0; k < nblocks; ++k) {
+      const uint32_t o0 = rd<uint32_t>(b.p, b.off_blocks + 4 * k), o1 = rd<uint32_t>(b.p, b.off_blocks + 4 * (k + 1));
+      if (o1 < o0 || b.off_codes + 16ull * o1 > b.off_blocks) { report[0]++; continue; }
+      uint64_t need = b.T;
+      for (uint32_t j = 0; j < b.T; ++j) {
+        const uint32_t m = b.p[b.off_codes + 16ull * o0 + j];
+        if (m > 63u) report[0]++;
+        for (int g = 0; g < 6; ++g) need += ((m >> g) & 1u) * (b.w / 8);
+      }
+      if (need > 16ull * (o1 - o0)) report[0]++;
+    }
+  }
   // subtree triangle sets, bottom-up (reverse DFS preorder), then containment
   for (auto it = order.rbegin(); it != order.rend(); ++it) {
     uint32_t n = *it;

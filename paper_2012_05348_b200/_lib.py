@@ -25,11 +25,11 @@ class cbvh_mesh(C.Structure):
 
 class cbvh_build_opts(C.Structure):
     _fields_ = [("treelet_nodes", C.c_int), ("leaf_size", C.c_int), ("layout", C.c_int), ("kdop", C.c_int),
-                ("align_treelets", C.c_int)]
+                ("align_treelets", C.c_int), ("zero_suppress", C.c_int)]
 
 
 CBVH_LAYOUT_DELTA, CBVH_LAYOUT_FP16, CBVH_LAYOUT_FP32 = 0, 1, 2
-CBVH_FLAG_ALIGNED_TREELETS = 1
+CBVH_FLAG_ALIGNED_TREELETS, CBVH_FLAG_ZERO_SUPPRESSED = 1, 2
 LAYOUTS = {"delta": CBVH_LAYOUT_DELTA, "fp16": CBVH_LAYOUT_FP16, "fp32": CBVH_LAYOUT_FP32}
 
 
@@ -41,7 +41,8 @@ class cbvh_header(C.Structure):
                 ("root_box", C.c_int32 * 6), ("off_topo", C.c_uint64), ("off_codes", C.c_uint64),
                 ("off_treelets", C.c_uint64), ("off_tris", C.c_uint64), ("off_tri_index", C.c_uint64),
                 ("total_bytes", C.c_uint64), ("layout", C.c_uint32), ("kdop", C.c_uint32),
-                ("off_axes", C.c_uint64), ("flags", C.c_uint32), ("real_nodes", C.c_uint32)]
+                ("off_axes", C.c_uint64), ("flags", C.c_uint32), ("real_nodes", C.c_uint32),
+                ("off_blocks", C.c_uint64)]
 
 
 class cbvh_info(C.Structure):

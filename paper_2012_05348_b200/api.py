@@ -58,13 +58,14 @@ def blob_info(blob: np.ndarray) -> dict:
                 off_tris=h.off_tris, off_tri_index=h.off_tri_index, total_bytes=h.total_bytes,
                 layout={v: k for k, v in L.LAYOUTS.items()}[h.layout], kdop=h.kdop, off_axes=h.off_axes,
                 aligned_treelets=bool(h.flags & L.CBVH_FLAG_ALIGNED_TREELETS), real_nodes=h.real_nodes,
+                zero_suppressed=bool(h.flags & L.CBVH_FLAG_ZERO_SUPPRESSED), off_blocks=h.off_blocks,
                 bvh_bytes=info.bvh_bytes, tri_bytes=info.tri_bytes, bytes_per_node=info.bytes_per_node,
                 code_bytes_per_node=info.code_bytes_per_node)
 
 
 def build_compressed_bvh(vertices, triangles, branching: int = 4, bits: int = 8,
                          treelet_nodes: int = 32, leaf_size: int = 4, layout: str = "delta",
-                         kdop: int = 6, align_treelets: bool = False) -> CompressedBVH:
+                         kdop: int = 6, align_treelets: bool = False, zero_suppress: bool = False) -> CompressedBVH:
     """C-ABI build_compressed_bvh: host BVH build, lattice quantization,
     predictor–corrector codes and treelet packing.
 
@@ -72,8 +73,11 @@ def build_compressed_bvh(vertices, triangles, branching: int = 4, bits: int = 8,
     boxes for the paper's half-vs-float comparison (§III.A).
     kdop: 6 (AABB) or 14 / 18 / 26 — k-DOP bounding volumes (Table I), delta
     coded per slab direction; used for the static model B.
-    align_treelets: treelet k occupies node ids [kT, kT + T) so the traversal
-    can stage whole treelet blocks in shared memory."""
+    align_treelets: whole treelets packed into T-slot blocks so the traversal
+    can stage treelet blocks in shared memory.
+    zero_suppress: integer-compressed corrections: per node a field
+    presence mask and only the non-zero fields; implies align_treelets, and
+    queries on such blobs decode from staged blocks."""
     if layout not in L.LAYOUTS:
         raise ValueError(f"layout must be one of {sorted(L.LAYOUTS)}")
     lib = L.load()
@@ -81,7 +85,8 @@ def build_compressed_bvh(vertices, triangles, branching: int = 4, bits: int = 8,
     t = np.ascontiguousarray(triangles, dtype=np.int32).reshape(-1, 3)
     mesh = L.cbvh_mesh(v.ctypes.data_as(C.POINTER(C.c_float)), len(v),
                        t.ctypes.data_as(C.POINTER(C.c_int32)), len(t))
-    opts = L.cbvh_build_opts(int(treelet_nodes), int(leaf_size), L.LAYOUTS[layout], int(kdop), int(bool(align_treelets)))
+    opts = L.cbvh_build_opts(int(treelet_nodes), int(leaf_size), L.LAYOUTS[layout], int(kdop), int(bool(align_treelets)),
+                             int(bool(zero_suppress)))
     out = C.POINTER(C.c_uint8)()
     n = C.c_size_t(0)
     L.check(lib.build_compressed_bvh(C.byref(mesh), int(branching), int(bits), C.byref(opts),

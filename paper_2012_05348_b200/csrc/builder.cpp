@@ -172,7 +172,10 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   if (kdop != 6 && layout != CBVH_LAYOUT_DELTA) return set_error(CBVH_EINVAL, "k-DOPs use the delta layout");
   if (layout != CBVH_LAYOUT_DELTA && layout != CBVH_LAYOUT_FP16 && layout != CBVH_LAYOUT_FP32)
     return set_error(CBVH_EINVAL, "layout must be CBVH_LAYOUT_DELTA, _FP16 or _FP32");
-  const bool aligned = opts && opts->align_treelets;
+  const bool aligned = opts && (opts->align_treelets || opts->zero_suppress);
+  const bool zs = opts && opts->zero_suppress;
+  if (zs && (bits <= 4 || layout != CBVH_LAYOUT_DELTA || kdop != 6))
+    return set_error(CBVH_EINVAL, "zero_suppress needs the delta AABB layout with 8- or 16-bit fields (bits > 4)");
   if (aligned && (T < 4 || T > 64 || (T & (T - 1)) || layout != CBVH_LAYOUT_DELTA || kdop != 6))
     return set_error(CBVH_EINVAL, "align_treelets needs the delta AABB layout and a power-of-two T in [4, 64]");
   if (!mesh->vertices || !mesh->triangles) return set_error(CBVH_EINVAL, "null mesh arrays");
@@ -475,9 +478,40 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
                    : bits <= 4 ? 4u : bits <= 8 ? 8u : 16u;
   const int nax = kdop / 2;
   const size_t code_bytes_node = 2 * (size_t)nax * w / 8;
+  // zero-suppressed codes (integer compression): per
+  // T-slot block a 16-byte aligned region = T field-presence masks (bit f:
+  // field f is non-zero) followed by the non-zero fields of the block's
+  // nodes in node and field order (w/8 bytes each); a table of region
+  // offsets (u32, 16-byte units from off_codes, one per block plus the end)
+  std::vector<uint8_t> zcodes;
+  std::vector<uint32_t> zoff;
+  if (zs) {
+    const int nblocks = nslots / T;
+    for (int b = 0; b < nblocks; ++b) {
+      zoff.push_back((uint32_t)(zcodes.size() / 16));
+      const size_t base = zcodes.size();
+      zcodes.resize(base + T, 0);
+      for (int j = 0; j < T; ++j) {
+        const int on = slot_node[(size_t)b * T + j];
+        if (on < 0) continue;
+        const uint16_t* q = &code[6 * (size_t)on];
+        uint8_t mask = 0;
+        for (int f = 0; f < 6; ++f) {
+          if (!q[f]) continue;
+          mask |= (uint8_t)(1u << f);
+          zcodes.push_back((uint8_t)(q[f] & 255u));
+          if (w == 16) zcodes.push_back((uint8_t)(q[f] >> 8));
+        }
+        zcodes[base + j] = mask;
+      }
+      zcodes.resize((zcodes.size() + 15) / 16 * 16, 0);
+    }
+    zoff.push_back((uint32_t)(zcodes.size() / 16));
+  }
   size_t off_topo = 256;
   size_t off_codes = align256(off_topo + 4 * (size_t)nslots);
-  size_t off_axes = align256(off_codes + code_bytes_node * (size_t)nslots);
+  size_t off_blocks = zs ? align256(off_codes + zcodes.size()) : 0;
+  size_t off_axes = zs ? align256(off_blocks + 4 * zoff.size()) : align256(off_codes + code_bytes_node * (size_t)nslots);
   size_t off_treelets = align256(off_axes + 16 * (size_t)nx);
   size_t off_tris = align256(off_treelets + 32 * treelets.size());
   size_t off_tri_index = align256(off_tris + 48 * (size_t)nt);
@@ -511,8 +545,13 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
   put<uint32_t>(out, 136, (uint32_t)layout);
   put<uint32_t>(out, 140, (uint32_t)kdop);
   put<uint64_t>(out, 144, off_axes);
-  put<uint32_t>(out, 152, aligned ? CBVH_FLAG_ALIGNED_TREELETS : 0u);
+  put<uint32_t>(out, 152, (aligned ? CBVH_FLAG_ALIGNED_TREELETS : 0u) | (zs ? CBVH_FLAG_ZERO_SUPPRESSED : 0u));
   put<uint32_t>(out, 156, (uint32_t)n);
+  put<uint64_t>(out, 160, off_blocks);
+  if (zs) {
+    std::memcpy(&out[off_codes], zcodes.data(), zcodes.size());
+    std::memcpy(&out[off_blocks], zoff.data(), 4 * zoff.size());
+  }
   for (int a = 0; a < nx; ++a) {
     const size_t o = off_axes + 16 * (size_t)a;
     put<float>(out, o, xorigin[a]);
@@ -521,7 +560,7 @@ int build_blob(const cbvh_mesh* mesh, int branching, int bits, const cbvh_build_
     put<int32_t>(out, o + 12, (int32_t)xroot[2 * a + 1]);
   }
   std::memcpy(&out[off_topo], topo.data(), 4 * (size_t)nslots);
-  for (int nid = 0; nid < nslots; ++nid) {
+  for (int nid = 0; nid < nslots && !zs; ++nid) {
     if (slot_node[nid] < 0) continue;  // padding: zero codes
     const int on = slot_node[nid];
     const uint16_t* q = &code[6 * (size_t)on];
@@ -582,7 +621,9 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
   h->off_axes = u64(144);
   h->flags = u32(152);
   h->real_nodes = u32(156);
-  if (h->flags & ~(uint32_t)CBVH_FLAG_ALIGNED_TREELETS) return set_error(CBVH_EBLOB, "unknown header flags");
+  h->off_blocks = u64(160);
+  if (h->flags & ~(uint32_t)(CBVH_FLAG_ALIGNED_TREELETS | CBVH_FLAG_ZERO_SUPPRESSED))
+    return set_error(CBVH_EBLOB, "unknown header flags");
   if (h->kdop != 6 && h->kdop != 14 && h->kdop != 18 && h->kdop != 26) return set_error(CBVH_EBLOB, "bad k");
   if (h->kdop != 6 && h->layout != CBVH_LAYOUT_DELTA) return set_error(CBVH_EBLOB, "k-DOP with an absolute layout");
   h->branching = u32(8); h->bits = u32(12); h->treelet_nodes = u32(16); h->leaf_size = u32(20);
@@ -602,8 +643,17 @@ int parse_header(const uint8_t* p, size_t bytes, cbvh_header* h) {
   if (h->num_nodes == 0 || h->num_tris == 0 || h->num_nodes >= (1u << 28) || h->num_tris >= (1u << 29))
     return set_error(CBVH_EBLOB, "bad counts");
   const uint64_t cb = (uint64_t)h->kdop * h->code_width / 8;
+  const bool zs = (h->flags & CBVH_FLAG_ZERO_SUPPRESSED) != 0;
+  if (zs && (!(h->flags & CBVH_FLAG_ALIGNED_TREELETS) || h->code_width < 8 || h->kdop != 6))
+    return set_error(CBVH_EBLOB, "bad zero-suppressed layout");
+  // zero-suppressed: codes section [off_codes, off_blocks), then the block
+  // offset table (num_nodes / T + 1 words) up to off_axes
+  const uint64_t code_end = zs ? h->off_blocks : h->off_codes + cb * h->num_nodes;
+  if (zs && (h->off_blocks < h->off_codes || (h->off_blocks & 15) ||
+             h->off_blocks + 4ull * (h->num_nodes / h->treelet_nodes + 1) > h->off_axes))
+    return set_error(CBVH_EBLOB, "bad section offsets");
   if (h->off_topo < 256 || h->off_topo + 4ull * h->num_nodes > h->off_codes ||
-      h->off_codes + cb * h->num_nodes > h->off_axes || h->off_axes + 16ull * (h->kdop / 2 - 3) > h->off_treelets ||
+      code_end > h->off_axes || h->off_axes + 16ull * (h->kdop / 2 - 3) > h->off_treelets ||
       h->off_treelets + 32ull * h->num_treelets > h->off_tris ||
       h->off_tris + 48ull * h->num_tris > h->off_tri_index ||
       h->off_tri_index + 4ull * h->num_tris > h->total_bytes)
@@ -657,6 +707,13 @@ int cbvh_blob_info(const uint8_t* h_blob, size_t bytes, cbvh_info* out) {
   // table; the treelet table (anchors) is build metadata the device never
   // reads, so it is not counted
   out->bvh_bytes = 4ull * h.num_nodes + ((uint64_t)h.kdop * h.code_width / 8) * h.num_nodes + 16ull * (h.kdop / 2 - 3);
+  if (h.flags & CBVH_FLAG_ZERO_SUPPRESSED) {
+    // the packed regions and their offset table
+    const uint64_t nblocks = h.num_nodes / h.treelet_nodes;
+    uint32_t end;
+    std::memcpy(&end, h_blob + h.off_blocks + 4 * nblocks, 4);
+    out->bvh_bytes = 4ull * h.num_nodes + 16ull * end + 4ull * (nblocks + 1);
+  }
   out->tri_bytes = 48ull * h.num_tris;
   out->bytes_per_node = (double)out->bvh_bytes / (double)h.real_nodes;
   out->code_bytes_per_node = (double)h.kdop * h.code_width / 8.0;

@@ -71,6 +71,8 @@ struct DevTree {
   int32_t root[6];   // decoded root lattice box
   int tlog;          // aligned treelet blocks: log2 T (node id = block << tlog | offset); -1: not staged
   int cb;            // code bytes per node (6 w / 8)
+  const uint32_t* zoff;  // zero-suppressed codes: per-block region offsets (16-byte units from codes); else null
+  int stage_ok;          // blocks can be staged (aligned, 16-byte multiples)
 };
 
 // k-DOP slab axes of the static model B beyond x, y, z (kdop/2 - 3 <= 10):
@@ -234,6 +236,41 @@ __device__ __forceinline__ void to_float_box(const DevTree& T, const int32_t C[6
   hi[2] = __fmaf_ru(__int2float_rn(C[5]), T.cell, T.oz);
 }
 
+// Zero-suppressed codes (integer compression): node j
+// of block b has presence mask m = region[j] (region = codes + 16 zoff[b]),
+// and its non-zero fields follow, in field order, at byte
+// T + (w/8) x (set bits of the masks of nodes 0..j-1).  From global memory
+// the prefix is a popcount over the preceding mask bytes (<= 16 words).
+__device__ __forceinline__ void load_codes_zs(const uint8_t* region, const uint8_t* fields0, uint32_t m, uint32_t before,
+                                              int width, uint32_t q[6]) {
+  const int wb = width >> 3;
+  const uint8_t* x = fields0 + wb * before;
+  #pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const bool on = (m >> f) & 1u;
+    const uint32_t v = on ? (wb == 2 ? (uint32_t)x[0] | ((uint32_t)x[1] << 8) : (uint32_t)x[0]) : 0u;
+    q[f] = v;
+    x += on ? wb : 0;
+  }
+  (void)region;
+}
+
+__device__ __forceinline__ void load_codes_zs_global(const uint8_t* codes, const uint32_t* zoff, int tlog, int width,
+                                                     uint32_t node, uint32_t q[6]) {
+  const uint32_t blk = node >> tlog, loc = node & ((1u << tlog) - 1u);
+  const uint8_t* region = codes + 16ull * __ldg(zoff + blk);
+  const uint32_t* mw = reinterpret_cast<const uint32_t*>(region);
+  uint32_t before = 0;
+  for (uint32_t k = 0; 4 * k < loc; ++k) {
+    uint32_t wv = __ldg(mw + k);
+    const uint32_t nb = loc - 4 * k;  // mask bytes of this word that precede node loc
+    if (nb < 4) wv &= (1u << (8 * nb)) - 1u;
+    before += __popc(wv);
+  }
+  const uint32_t m = __ldg(region + loc);
+  load_codes_zs(region, region + (1u << tlog), m, before, width, q);
+}
+
 // ---------------------------------------------------------------- node boxes
 // A node's box travels as 6 words: lattice ints (DELTA) or fp32 bits
 // (FP16 / FP32, absolute).  The child box comes from the parent's words
@@ -241,7 +278,8 @@ __device__ __forceinline__ void to_float_box(const DevTree& T, const int32_t C[6
 __device__ __forceinline__ void fetch_child_box(const DevTree& T, uint32_t node, const int32_t P[6], int32_t C[6]) {
   if (T.layout == CBVH_LAYOUT_DELTA) {
     uint32_t q[6];
-    load_codes(T, node, q);
+    if (T.zoff) load_codes_zs_global(T.codes, T.zoff, T.tlog, T.width, node, q);
+    else load_codes(T, node, q);
     decode_child(P, q, T.bits, C);
   } else if (T.layout == CBVH_LAYOUT_FP16) {
     // binary16 descriptors (§III.A): widened exactly to fp32
@@ -1148,11 +1186,23 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 // T; returns the lane's slot or -1 (no node, or no free slot: read global).
 // All misses of the pass are copied together with asynchronous 16-byte
 // global->shared copies (cp.async, LDGSTS), so their latencies overlap.
+// Slot layout (words): T topology words; the codes (T x cb bytes, or a
+// zero-suppressed region of at most T + 6 T w/8 bytes); zero-suppressed only:
+// T u16 byte offsets of each node's first field within the region.
+__host__ __device__ __forceinline__ int region_words(const DevTree& T) {
+  const int n = 1 << T.tlog;
+  return T.zoff ? ((n + 6 * n * (T.width >> 3) + 15) / 16) * 4 : (n * T.cb) / 4;
+}
+__host__ __device__ __forceinline__ int slot_words(const DevTree& T) {
+  const int n = 1 << T.tlog;
+  return n + region_words(T) + (T.zoff ? n / 2 : 0);
+}
+
 template <bool STATS>
 __device__ __forceinline__ int stage_block(const Params& p, const WarpCtx& c, const DevTree& T, uint32_t tree_bit,
                                            uint32_t node, unsigned* used, unsigned* rr,
                                            unsigned long long* s_blocks, unsigned long long* s_bytes) {
-  const uint32_t key = (node == kNoBlock || T.tlog < 0) ? kNoBlock : ((node >> T.tlog) | tree_bit);
+  const uint32_t key = (node == kNoBlock || !T.stage_ok) ? kNoBlock : ((node >> T.tlog) | tree_bit);
   if (!__any_sync(FULL, key != kNoBlock)) return -1;
   const unsigned grp = __match_any_sync(FULL, key);
   const int leader = __ffs(grp) - 1;
@@ -1189,18 +1239,48 @@ __device__ __forceinline__ int stage_block(const Params& p, const WarpCtx& c, co
       ++nfill;
     }
     __syncwarp();  // the new tags are visible to every lane
-    // copy: nfill blocks x (nt + nc) 16-byte chunks, spread over the lanes
-    const int nt = (1 << T.tlog) >> 2, nc = ((1 << T.tlog) * T.cb) >> 4, per = nt + nc;
-    for (int q = c.lane; q < nfill * per; q += 32) {
-      const int b = q / per, r = q - b * per;
+    // copy: per block nt topology chunks + its code chunks (16 bytes each),
+    // all blocks' copies in flight together
+    const int nt = (1 << T.tlog) >> 2;
+    unsigned long long bytes = 0;
+    for (int b = 0; b < nfill; ++b) {
       const int v = (int)((fill >> (8 * b)) & 255u);
-      const size_t first = (size_t)(c.stag[v] & ~kTreeB) << T.tlog;
-      const void* src = r < nt ? static_cast<const void*>(T.topo + first + 4 * r)
-                               : static_cast<const void*>(T.codes + first * T.cb + 16 * (r - nt));
-      cp_async16(c.stg + v * p.stage_slot_words + 4 * r, src);
+      const uint32_t blk = c.stag[v] & ~kTreeB;
+      const size_t first = (size_t)blk << T.tlog;
+      const uint8_t* csrc = T.zoff ? T.codes + 16ull * __ldg(T.zoff + blk) : T.codes + first * T.cb;
+      const int nc = T.zoff ? (int)(__ldg(T.zoff + blk + 1) - __ldg(T.zoff + blk)) : ((1 << T.tlog) * T.cb) >> 4;
+      uint32_t* dst = c.stg + v * p.stage_slot_words;
+      for (int q = c.lane; q < nt + nc; q += 32)
+        cp_async16(dst + 4 * q, q < nt ? static_cast<const void*>(T.topo + first + 4 * q)
+                                       : static_cast<const void*>(csrc + 16 * (q - nt)));
+      bytes += 16ull * (nt + nc);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-    if (STATS && c.lane == 0) { *s_blocks += nfill; *s_bytes += 16ull * per * nfill; }
+    if (T.zoff) {
+      // zero-suppressed: each node's field offset = T + (w/8) x (set mask
+      // bits of the nodes before it), a warp prefix sum over the masks
+      __syncwarp();
+      const int n = 1 << T.tlog, wb = T.width >> 3;
+      for (int b = 0; b < nfill; ++b) {
+        uint32_t* slotp = c.stg + ((fill >> (8 * b)) & 255u) * p.stage_slot_words;
+        const uint8_t* reg = reinterpret_cast<const uint8_t*>(slotp + n);
+        unsigned short* offs = reinterpret_cast<unsigned short*>(slotp + n + region_words(T));
+        uint32_t carry = 0;
+        for (int h = 0; h < n; h += 32) {
+          const int j = h + c.lane;
+          const uint32_t x = j < n ? (uint32_t)__popc(reg[j]) : 0u;
+          uint32_t inc = x;
+          #pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, inc, o);
+            if (c.lane >= o) inc += y;
+          }
+          if (j < n) offs[j] = (unsigned short)(n + wb * (carry + inc - x));
+          carry += __shfl_sync(FULL, inc, 31);
+        }
+      }
+    }
+    if (STATS && c.lane == 0) { *s_blocks += nfill; *s_bytes += bytes; }
   }
   __syncwarp();
   s = __shfl_sync(FULL, s, leader);
@@ -1231,8 +1311,14 @@ __device__ __forceinline__ uint32_t fetch_child(const WarpCtx& c, const Params& 
   if (slot >= 0) {
     const uint32_t* blk = c.stg + slot * p.stage_slot_words;
     const uint32_t loc = node & ((1u << T.tlog) - 1u);
+    const uint8_t* reg = reinterpret_cast<const uint8_t*>(blk + (1 << T.tlog));
     uint32_t q[6];
-    load_codes_at(reinterpret_cast<const uint8_t*>(blk + (1 << T.tlog)) + loc * T.cb, T.width, q);
+    if (T.zoff) {
+      const unsigned short* offs = reinterpret_cast<const unsigned short*>(blk + (1 << T.tlog) + region_words(T));
+      load_codes_zs(reg, reg + offs[loc], reg[loc], 0u, T.width, q);
+    } else {
+      load_codes_at(reg + loc * T.cb, T.width, q);
+    }
     decode_child(P, q, T.bits, C);
     return blk[loc];
   }
@@ -2241,10 +2327,14 @@ static DevTree make_tree(const cbvh_bvh* T) {
   d.n_tris = h.num_tris;
   d.cb = (int)(h.kdop * h.code_width / 8);
   d.tlog = -1;
+  d.stage_ok = 0;
+  d.zoff = nullptr;
   const uint32_t Tn = h.treelet_nodes;
-  if ((h.flags & CBVH_FLAG_ALIGNED_TREELETS) && h.kdop == 6 && Tn >= 4 && (Tn & (Tn - 1)) == 0 &&
-      (Tn * (uint32_t)d.cb) % 16 == 0)
+  if ((h.flags & CBVH_FLAG_ALIGNED_TREELETS) && h.kdop == 6 && Tn >= 4 && (Tn & (Tn - 1)) == 0) {
     for (d.tlog = 0; (1u << d.tlog) < Tn; ++d.tlog) {}
+    if (h.flags & CBVH_FLAG_ZERO_SUPPRESSED) d.zoff = reinterpret_cast<const uint32_t*>(base + h.off_blocks);
+    d.stage_ok = (d.zoff || (Tn * (uint32_t)d.cb) % 16 == 0) ? 1 : 0;
+  }
   return d;
 }
 
@@ -2268,7 +2358,7 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   p.B = make_tree(B);
   // treelet staging (KX = 0 only): the slot holds the larger of the two
   // trees' blocks; a tree whose blob is not aligned is read from global memory
-  if (KX != 0 || (p.A.tlog < 0 && p.B.tlog < 0)) stage = 0;
+  if (KX != 0 || (!p.A.stage_ok && !p.B.stage_ok)) stage = 0;
   p.stage_slot_words = 0;
   static const int sides = [] {
     const char* env = std::getenv("CBVH_STAGE_SIDES");
@@ -2276,7 +2366,7 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   }();
   p.stage_sides = sides;
   for (const DevTree* T : {&p.A, &p.B})
-    if (stage && T->tlog >= 0) p.stage_slot_words = std::max(p.stage_slot_words, ((1 << T->tlog) * (4 + T->cb)) / 4);
+    if (stage && T->stage_ok) p.stage_slot_words = std::max(p.stage_slot_words, slot_words(*T));
   const size_t smem = smem_bytes(MODE, KX) +
                       (stage ? (size_t)kWarps * (kStageTagWords + kStageSlots * p.stage_slot_words) * sizeof(uint32_t) : 0);
   LaunchShape s;
@@ -2422,6 +2512,27 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
       }
     }
     if (real != h.real_nodes || (padded && topo_at(0) == kPadTopo)) return set_error(CBVH_EBLOB, "bad node count");
+    if (h.flags & CBVH_FLAG_ZERO_SUPPRESSED) {
+      // block regions in order, inside the codes section, each holding its
+      // T masks (6 bits) and the fields they announce
+      const uint64_t T = h.treelet_nodes, nblocks = h.num_nodes / T, wb = h.code_width / 8;
+      const uint8_t* tab = h_blob + h.off_blocks;
+      uint32_t prev = 0;
+      for (uint64_t b = 0; b < nblocks; ++b) {
+        uint32_t o0, o1;
+        std::memcpy(&o0, tab + 4 * b, 4);
+        std::memcpy(&o1, tab + 4 * (b + 1), 4);
+        if (o0 != prev || o1 < o0 || 16ull * o1 > h.off_blocks - h.off_codes) return set_error(CBVH_EBLOB, "bad code regions");
+        prev = o1;
+        const uint8_t* r = h_blob + h.off_codes + 16ull * o0;
+        uint64_t need = T;
+        for (uint64_t j = 0; j < T; ++j) {
+          if (r[j] > 63u || (r[j] && topo_at(b * T + j) == kPadTopo)) return set_error(CBVH_EBLOB, "bad presence mask");
+          need += wb * (uint64_t)__builtin_popcount(r[j]);
+        }
+        if (need > 16ull * (o1 - o0)) return set_error(CBVH_EBLOB, "bad code regions");
+      }
+    }
   }
   std::memset(out, 0, sizeof *out);
   out->d_blob = d_blob;
@@ -2453,7 +2564,14 @@ int cbvh_bind(const uint8_t* h_blob, size_t bytes, const void* d_blob, cbvh_bvh*
   // lo of the k/2 axes, then hi (4-bit fields two per byte, low nibble first).
   const int nax = (int)h.kdop / 2;
   const uint8_t* c = h_blob + h.off_codes;
+  const bool zs = (h.flags & CBVH_FLAG_ZERO_SUPPRESSED) != 0;
   auto field = [&](int f) -> uint32_t {
+    if (zs) {  // node 0 = slot 0 of block 0 (region offset 0): mask byte, then its non-zero fields
+      const uint32_t m = c[0];
+      if (!((m >> f) & 1u)) return 0u;
+      const uint8_t* x = c + h.treelet_nodes + (h.code_width / 8) * __builtin_popcount(m & ((1u << f) - 1u));
+      return h.code_width == 16 ? (uint32_t)x[0] | ((uint32_t)x[1] << 8) : x[0];
+    }
     if (h.code_width == 16) { uint16_t x; std::memcpy(&x, c + 2 * f, 2); return x; }
     if (h.code_width == 8) return c[f];
     return (c[f / 2] >> (4 * (f % 2))) & 15u;

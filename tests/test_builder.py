@@ -111,6 +111,62 @@ def test_aligned_treelets(cfg1, mesh16k, B, bits, T):
         assert O.collide_pairs(ta, tb, p) == O.collide_pairs(ra, rb, p)
 
 
+@pytest.mark.parametrize("B,bits,T", [(2, 8, 32), (4, 8, 32), (4, 8, 64), (8, 16, 64), (4, 12, 16)])
+def test_zero_suppressed_codes(cfg1, mesh16k, B, bits, T):
+    # integer-compressed corrections: the oracle's own decoder of the
+    # presence-mask format (oracle.cpp code_field) finds every box containing
+    # its subtree, the pair sets equal the plain blob's, and the codes shrink
+    for m in (cfg1.A, mesh16k):
+        z = M.build_compressed_bvh(m.vertices, m.triangles, B, bits, T, 4, zero_suppress=True)
+        al = M.build_compressed_bvh(m.vertices, m.triangles, B, bits, T, 4, align_treelets=True)
+        r = O.check_blob(z.blob, m.vertices, m.triangles)
+        assert r["violations"] == 0, r
+        assert z.info["zero_suppressed"] and z.info["aligned_treelets"]
+        assert z.info["num_nodes"] == al.info["num_nodes"] and z.info["real_nodes"] == al.info["real_nodes"]
+        # at b = 8 zero corrections are common (a child sharing a parent
+        # face) and each saves a byte: fewer hierarchy bytes than the same
+        # aligned blob (at b = 16 the corrections rarely vanish)
+        if bits == 8:
+            assert z.info["bvh_bytes"] < al.info["bvh_bytes"]
+    A, Bm, P = cfg1.A, cfg1.B, cfg1.poses[:24]
+    ta = O.Tree.from_blob(M.build_compressed_bvh(A.vertices, A.triangles, B, bits, T, 4, zero_suppress=True).blob,
+                          A.vertices, A.triangles)
+    tb = O.Tree.from_blob(M.build_compressed_bvh(Bm.vertices, Bm.triangles, B, bits, T, 4, zero_suppress=True).blob,
+                          Bm.vertices, Bm.triangles)
+    ra, rb = O.Tree.from_mesh(A.vertices, A.triangles), O.Tree.from_mesh(Bm.vertices, Bm.triangles)
+    for p in P:
+        assert O.collide_pairs(ta, tb, p) == O.collide_pairs(ra, rb, p)
+
+
+def test_zero_suppressed_errors_and_faults(cfg1):
+    A = cfg1.A
+    for kw in (dict(bits=4), dict(layout="fp16"), dict(kdop=14)):
+        bits = kw.pop("bits", 8)
+        with pytest.raises(L.CbvhError, match="EINVAL"):
+            M.build_compressed_bvh(A.vertices, A.triangles, 4, bits, zero_suppress=True, **kw)
+    z = M.build_compressed_bvh(A.vertices, A.triangles, 4, 8, 32, 4, zero_suppress=True)
+    i = z.info
+    region0 = i["off_codes"]
+    lib = L.load()
+    out = L.cbvh_bvh()
+
+    def bind(blob):
+        return lib.cbvh_bind(blob.ctypes.data_as(C.POINTER(C.c_uint8)), blob.nbytes, C.c_void_p(1 << 20), C.byref(out))
+
+    assert bind(z.blob) == L.CBVH_OK
+    # a presence mask with a 7th bit, and a mask that announces a field the
+    # region does not hold, are rejected by bind and flagged by the checker
+    bad = z.blob.copy()
+    bad[region0 + 1] |= 64
+    assert bind(bad) == L.CBVH_EBLOB
+    assert O.check_blob(bad, A.vertices, A.triangles)["malformed"] > 0
+    # flipping a mask bit shifts every later field: boxes decode wrong
+    bad = z.blob.copy()
+    j = next(k for k in range(1, 32) if bad[region0 + k] not in (0, 63))
+    bad[region0 + j] ^= next(1 << f for f in range(6) if not (bad[region0 + j] >> f) & 1)
+    assert O.check_blob(bad, A.vertices, A.triangles)["violations"] > 0
+
+
 def test_aligned_treelets_errors_and_faults(cfg1):
     A = cfg1.A
     for kw in (dict(treelet_nodes=48), dict(treelet_nodes=128), dict(layout="fp32"), dict(kdop=14)):

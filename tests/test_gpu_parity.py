@@ -53,9 +53,9 @@ def run_distance(M, A, B, poses, stats=False, descent="larger"):
     return out
 
 
-def build(M, mesh, B, bits, T=32, layout="delta", kdop=6, aligned=False):
+def build(M, mesh, B, bits, T=32, layout="delta", kdop=6, aligned=False, zs=False):
     return M.build_compressed_bvh(mesh.vertices, mesh.triangles, B, bits, T, 4, layout=layout,
-                                  kdop=kdop, align_treelets=aligned).to_device()
+                                  kdop=kdop, align_treelets=aligned, zero_suppress=zs).to_device()
 
 
 def run_collide_staged(M, A, B, poses, staging):
@@ -266,6 +266,25 @@ def test_config1_treelet_staging(M, cfg1, Bf, bits, T):
     check_distance(d, d64, delta, f"staged distance B={Bf}")
     with pytest.raises(M._lib.CbvhError, match="EINVAL"):
         M.collide_batch(build(M, w.A, Bf, bits, T), build(M, w.B, Bf, bits, T), P, staging="on")
+
+
+@pytest.mark.parametrize("Bf,bits,T", [(2, 8, 32), (4, 8, 64), (8, 16, 64), (4, 12, 16)])
+def test_config1_zero_suppressed_codes(M, cfg1, Bf, bits, T):
+    # integer-compressed corrections: decoded from staged blocks and,
+    # unstaged, straight from global memory (mask popcounts) — both in band
+    # vs the oracle and identical to the plain aligned blob's counts
+    w, tA, tB, delta, cnt, H, Z = cfg1
+    A, B = build(M, w.A, Bf, bits, T, zs=True), build(M, w.B, Bf, bits, T, zs=True)
+    ref = run_collide(M, build(M, w.A, Bf, bits, T, aligned=True), build(M, w.B, Bf, bits, T, aligned=True), w.poses)
+    for staging in ("on", "off"):
+        hit, gc, st = run_collide_staged(M, A, B, w.poses, staging)
+        check_collide(hit, gc, H, Z, f"zero-suppressed {staging} B={Bf} b={bits}")
+        assert np.array_equal(gc, ref[1])
+        assert (st["treelet_blocks"] > 0) == (staging == "on")
+    P = torch.from_numpy(w.poses[:256]).cuda()
+    d64, _ = O.distance(tA, tB, w.poses[:256])
+    for staging in ("on", "off"):
+        check_distance(M.distance_batch(A, B, P, staging=staging).cpu().numpy(), d64, delta, f"zs distance {staging}")
 
 
 @pytest.mark.parametrize("k", [1, 3])
@@ -525,6 +544,19 @@ def test_config5_treelet_staging_full_size(M):
     assert np.array_equal(c1, c0) and np.array_equal(h1, h0)
     assert s1["treelet_blocks"] > 0 and s1["bv_tests"] == s0["bv_tests"]
     print("cfg5 staging", {k: s1[k] for k in ("treelet_blocks", "treelet_bytes", "staged_reads", "nodes_decoded")})
+
+
+def test_config5_zero_suppressed_full_size(M):
+    # full config 5 batch, zero-suppressed blobs: staged and unstaged decode
+    # give the packed blob's counts on every pose
+    w = G.make_config(5)
+    _, ref = run_collide(M, build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet),
+                         w.poses)
+    A = build(M, w.A, w.branching, w.bits, w.treelet, zs=True)
+    B = build(M, w.B, w.branching, w.bits, w.treelet, zs=True)
+    for staging in ("on", "off"):
+        _, gc, _ = run_collide_staged(M, A, B, w.poses, staging)
+        assert np.array_equal(gc, ref), staging
 
 
 def test_config5_early_exit_full_size(M):
