@@ -236,6 +236,9 @@ __device__ __forceinline__ void to_float_box(const DevTree& T, const int32_t C[6
   hi[2] = __fmaf_ru(__int2float_rn(C[5]), T.cell, T.oz);
 }
 
+#ifndef CBVH_ZS
+#define CBVH_ZS 1
+#endif
 // Zero-suppressed codes (integer compression): node j
 // of block b has presence mask m = region[j] (region = codes + 16 zoff[b]),
 // and its non-zero fields follow, in field order, at byte
@@ -255,8 +258,10 @@ __device__ __forceinline__ void load_codes_zs(const uint8_t* region, const uint8
   (void)region;
 }
 
-__device__ __forceinline__ void load_codes_zs_global(const uint8_t* codes, const uint32_t* zoff, int tlog, int width,
-                                                     uint32_t node, uint32_t q[6]) {
+// (returns the six fields packed in pairs, q0 | q1 << 16 ..., in registers)
+__device__ __noinline__ uint3 load_codes_zs_global(const uint8_t* codes, const uint32_t* zoff, int tlog, int width,
+                                                   uint32_t node) {
+  uint32_t q[6];
   const uint32_t blk = node >> tlog, loc = node & ((1u << tlog) - 1u);
   const uint8_t* region = codes + 16ull * __ldg(zoff + blk);
   const uint32_t* mw = reinterpret_cast<const uint32_t*>(region);
@@ -269,6 +274,7 @@ __device__ __forceinline__ void load_codes_zs_global(const uint8_t* codes, const
   }
   const uint32_t m = __ldg(region + loc);
   load_codes_zs(region, region + (1u << tlog), m, before, width, q);
+  return make_uint3(q[0] | (q[1] << 16), q[2] | (q[3] << 16), q[4] | (q[5] << 16));
 }
 
 // ---------------------------------------------------------------- node boxes
@@ -278,8 +284,14 @@ __device__ __forceinline__ void load_codes_zs_global(const uint8_t* codes, const
 __device__ __forceinline__ void fetch_child_box(const DevTree& T, uint32_t node, const int32_t P[6], int32_t C[6]) {
   if (T.layout == CBVH_LAYOUT_DELTA) {
     uint32_t q[6];
-    if (T.zoff) load_codes_zs_global(T.codes, T.zoff, T.tlog, T.width, node, q);
-    else load_codes(T, node, q);
+    // (zero-suppressed blobs: an out-of-line call, so the common path keeps
+    // its registers and code layout; CBVH_ZS=0 builds without the branch)
+    if (CBVH_ZS && T.zoff) {
+      const uint3 z = load_codes_zs_global(T.codes, T.zoff, T.tlog, T.width, node);
+      q[0] = z.x & 0xffffu; q[1] = z.x >> 16; q[2] = z.y & 0xffffu; q[3] = z.y >> 16; q[4] = z.z & 0xffffu; q[5] = z.z >> 16;
+    } else {
+      load_codes(T, node, q);
+    }
     decode_child(P, q, T.bits, C);
   } else if (T.layout == CBVH_LAYOUT_FP16) {
     // binary16 descriptors (§III.A): widened exactly to fp32

@@ -381,6 +381,22 @@ def test_error_paths_device(M, cfg1):
     M.collide_batch(A, B, P, workspace=ws)
     M.check(ws)
     assert M.last_launch_count() >= 2  # init + the load-balancing phases
+    # the binding checks caller buffers before any kernel writes through them
+    with pytest.raises(ValueError):
+        M.collide_batch(A, B, P, hit=torch.empty(10, dtype=torch.uint8, device="cuda"), workspace=ws)
+    with pytest.raises(TypeError):
+        M.collide_batch(A, B, P, count=torch.empty(64, dtype=torch.float32, device="cuda"), workspace=ws)
+    with pytest.raises(ValueError):
+        M.distance_batch(A, B, P, dist=torch.empty(64, dtype=torch.float32), workspace=M.Workspace(A, B, 1))
+    with pytest.raises(ValueError):
+        M.collide_batch(A, M.build_compressed_bvh(w.B.vertices, w.B.triangles, 2, 8), P)  # not on the device
+    # a call-local workspace on a side stream: the result is checked and synchronised before returning
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        hit, cnt = M.collide_batch(A, B, P, stream=side)
+    ref_hit, ref_cnt = M.collide_batch(A, B, P, workspace=ws)
+    M.check(ws)
+    assert torch.equal(cnt, ref_cnt) and torch.equal(hit, ref_hit)
 
 
 # ------------------------------------------------------------------ full-size configs, sampled

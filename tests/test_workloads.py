@@ -58,3 +58,23 @@ def test_validate_poses():
     P[7, 5] = np.nan          # not finite
     P[9, [0, 5, 10]] = [-1, -1, -1]   # reflection (det = -1)
     assert list(M.validate_poses(P)) == [3, 7, 9]
+
+
+@pytest.mark.parametrize("k,n", [(1, 96), (3, 12)])
+def test_zero_preset_table_is_the_oracles(k, n):
+    # the zero-separation preset stores the
+    # translation magnitudes tools/make_zero_preset.py bisected with the
+    # oracle: re-evaluated here, the oracle distance of the generated fp32
+    # poses equals the stored one and lies in (0, 1e-3)
+    import os
+    import oracle as O
+    w = G.make_config(k, num_poses=n, preset="zero")
+    tab = np.load(os.path.join(G.PRESET_DIR, f"zero_cfg{k}.npz"))
+    assert len(tab["s"]) == (1024 if k == 1 else 32768)
+    assert np.all((tab["distance"] > 0) & (tab["distance"] < 1e-3))
+    tA = O.Tree.from_mesh(w.A.vertices, w.A.triangles)
+    tB = O.Tree.from_mesh(w.B.vertices, w.B.triangles)
+    d, _ = O.distance(tA, tB, w.poses)
+    assert np.array_equal(d, tab["distance"][:n])
+    # the rotation and direction are the seeded draws; |t| is the table's s
+    assert np.allclose(np.linalg.norm(w.poses[:, [3, 7, 11]].astype(np.float64), axis=1), tab["s"][:n], rtol=1e-6)
