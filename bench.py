@@ -214,6 +214,51 @@ def l2_peak() -> dict | None:
                       "L2-resident buffer (best of L2/8, L2/4, L2/2), CUDA events"}
 
 
+CSV_COLUMNS = ("config", "workload", "mode", "poses", "branching", "bits", "treelet_nodes", "layout", "kdop_B", "seed",
+               "steps", "ms_per_step", "poses_per_s", "e2e_poses_per_s", "bv_tests_per_s", "bytes_per_node_A",
+               "bytes_per_node_B", "roofline_hbm_frac", "roofline_l2_frac", "roofline_issue_frac", "parity_status",
+               "parity_poses", "band_pairs", "poses_with_band", "max_rel_err", "oracle_poses_per_s", "oracle_cores",
+               "cpu_model", "sm_mhz")
+
+
+def write_csv(path: str, line: dict, args) -> None:
+    """One row per run (SURVEY §5 metrics: poses/s, BV tests/s, bytes/node,
+    roofline fractions, band counts, oracle time, cores), appended to `path`."""
+    import csv
+    c, par, cpu = line["config"], line.get("parity") or {}, line.get("cpu_baseline") or {}
+    row = {"config": args.config, "workload": c["workload"], "mode": "distance" if "proximity" in line["metric"] else "collide",
+           "poses": c["poses_per_gpu"], "branching": c["branching"], "bits": c["bits"], "treelet_nodes": c["treelet_nodes"],
+           "layout": c["layout"], "kdop_B": c["kdop_B"], "seed": args.seed, "steps": line["steps"],
+           "ms_per_step": line["ms_per_step"], "poses_per_s": line["value"], "e2e_poses_per_s": line["e2e"]["value"],
+           "bv_tests_per_s": line["bv_pair_tests_per_s"], "bytes_per_node_A": line["bytes_per_node"]["A"],
+           "bytes_per_node_B": line["bytes_per_node"]["B"], "roofline_hbm_frac": line["roofline"]["frac"],
+           "roofline_l2_frac": (line.get("roofline_l2") or {}).get("frac"),
+           "roofline_issue_frac": (line.get("roofline_issue") or {}).get("frac"),
+           "parity_status": par.get("status"), "parity_poses": par.get("poses_checked"),
+           "band_pairs": par.get("band_pairs"), "poses_with_band": par.get("poses_with_band"),
+           "max_rel_err": par.get("max_rel_err"), "oracle_poses_per_s": cpu.get("value"), "oracle_cores": cpu.get("cores"),
+           "cpu_model": cpu.get("cpu_model"), "sm_mhz": (line.get("clocks") or {}).get("sm_mhz")}
+    new = not os.path.exists(path) or os.path.getsize(path) == 0
+    with open(path, "a", newline="") as f:
+        wr = csv.DictWriter(f, fieldnames=CSV_COLUMNS)
+        if new:
+            wr.writeheader()
+        wr.writerow(row)
+
+
+def run_ncu(args, argv) -> int:
+    """--ncu: after the plain run exited 0, the same command once more under
+    ncu (a separate process; its printed numbers are not bench values) for the
+    per-launch list: duration, warp / thread instructions, L2 and DRAM bytes."""
+    out = args.ncu if args.ncu.endswith(".csv") else os.path.join(args.ncu, f"launches_cfg{args.config}.csv")
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    rest = [a for i, a in enumerate(argv) if a != "--ncu" and (i == 0 or argv[i - 1] != "--ncu")]
+    cmd = ["ncu", "--metrics", "gpu__time_duration.sum,smsp__inst_executed.sum,smsp__thread_inst_executed.sum,"
+           "lts__t_bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none", "-c", "400",
+           "--csv", "--log-file", out, sys.executable, os.path.abspath(__file__), *rest, "--no-cpu", "--quick"]
+    return subprocess.call(cmd, stdout=subprocess.DEVNULL)
+
+
 def run_reference(args):
     """--impl reference: the oracle on the host cores, same config/metric."""
     rank = _env_int("RANK", 0)
@@ -264,8 +309,10 @@ def run(args):
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
 
-    w = rank_workload(args.config, rank, args.poses, args.preset)
+    w = rank_workload(args.config, rank + args.seed, args.poses, args.preset)
     N = len(w.poses)
+    if args.treelet:
+        w.treelet = args.treelet
     t0 = time.time()
     if args.leaf:
         w.leaf = args.leaf
@@ -408,7 +455,8 @@ def run(args):
 
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_oracle_rate(w, n_sample=args.cpu_poses, budget_s=args.cpu_budget, distance=distance)
+        cpu = cpu_oracle_rate(w, n_sample=args.cpu_poses, nthreads=args.oracle_threads, budget_s=args.cpu_budget,
+                              distance=distance)
         parity = bench_parity(cpu, hit, cnt, dst, distance)
     l2 = l2_peak() if rank == 0 else None
 
@@ -465,6 +513,8 @@ def run(args):
             line["cpu_baseline"] = {k: v for k, v in cpu.items() if k in ("value", "unit", "cores", "kind", "sample",
                                                                           "cpu_model")}
         print(json.dumps(line), flush=True)
+        if args.csv:
+            write_csv(args.csv, line, args)
     if dist:
         dist.destroy_process_group()
 
@@ -500,16 +550,27 @@ def main():
                     help="integer-compressed corrections (presence masks; implies aligned treelet blocks)")
     ap.add_argument("--staging", default="auto", choices=["auto", "on", "off"],
                     help="treelet staging in shared memory (auto: when the blobs are aligned)")
+    ap.add_argument("--treelet", type=int, default=0, help="override the treelet size T (nodes)")
+    ap.add_argument("--seed", type=int, default=0, help="offset added to the config's pose seed (another pose batch)")
+    ap.add_argument("--repeat", type=int, default=0, help="alias of --steps (timed repetitions)")
+    ap.add_argument("--oracle-threads", type=int, default=0, help="host threads of the cpu_baseline oracle leg (0: all)")
+    ap.add_argument("--csv", default="", help="append one CSV row of this run's metrics to this file")
+    ap.add_argument("--ncu", default="", help="after the run, repeat it under ncu (separate process) and write the "
+                                              "per-launch list to this .csv (or directory)")
     ap.add_argument("--cpu-poses", type=int, default=100000)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-poses", type=int, default=2048, help="poses per --impl reference step")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.repeat:
+        args.steps = args.repeat
     if args.impl == "reference":
         run_reference(args)
     else:
         run(args)
+        if args.ncu and _env_int("WORLD_SIZE", 1) == 1:
+            run_ncu(args, sys.argv[1:])
 
 
 if __name__ == "__main__":
