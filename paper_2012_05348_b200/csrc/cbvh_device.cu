@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <utility>
 #include <atomic>
 
 #include <cfloat>
@@ -160,6 +161,7 @@ struct Params {
   int capped;            // distance: dist holds per-pose caps on entry (cbvh_query_opts.capped)
   int stage_slot_words;  // staging: words per smem slot (one treelet block: T topology words + T x cb code bytes)
   int stage_sides;       // staging: bit 0 tree A, bit 1 tree B (CBVH_STAGE_SIDES, tuning; default both)
+  int bmax;              // the larger branching factor of the two trees (warp dive: lanes per beam entry)
 };
 
 // item pose word: bits 0..29 pose id, bit 30 = descend a, bit 31 = descend b
@@ -186,6 +188,12 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+
+// Programmatic dependent launch (sm_90+): wait until the previous kernel of
+// the stream has completed and its writes are visible; let the next kernel's
+// CTAs become resident as soon as there is room for them.
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -1093,110 +1101,141 @@ __device__ __forceinline__ float pair_distance(const Params& p, const PoseF& P, 
   return d;
 }
 
-// Greedy dive (distance): one pose per thread runs a beam search of width W
-// from the root pair — each step expands every beam entry (the larger-first
-// side, or the non-leaf side), scores the children by the box lower bound and
-// keeps the W best; a kept leaf pair is evaluated (its triangle pairs'
-// distances, computed exactly as the leaf phase computes them) and leaves the
-// beam.  The smallest distance found becomes the pose's starting best.  These
-// are distances of real triangle pairs, so the traversal's result is unchanged
-// (min over a superset of the same values); it only prunes from the start
-// instead of from +inf (reading R26).
-template <int KX>
-struct DiveEntry {
-  uint32_t ta, tb;
-  float lb;
-  int32_t BA[6], BB[6], BX[2 * KX + 1];
-};
-
-template <int KX>
-__device__ __forceinline__ float dive_leaf_pair(const Params& p, const PoseF& P, uint32_t ta, uint32_t tb) {
+// Greedy dive (distance): a beam search from the root pair — each step
+// expands every beam entry (the larger-first side, or the non-leaf side),
+// scores the children by the box lower bound and keeps the W best; a kept leaf
+// pair is evaluated (its triangle pairs' distances, computed exactly as the
+// leaf phase computes them) and leaves the beam.  The smallest distance found
+// becomes the pose's starting best.  These are distances of real triangle
+// pairs, so the traversal's result is unchanged (min over a superset of the
+// same values); it only prunes from the start instead of from +inf (R26).
+// One warp per pose: the beam lives in shared memory and the lanes expand all
+// of its entries' children at once (lane = entry x child; W = 8 entries of
+// <= 4 children, or 4 of <= 8), the kept candidates are the W smallest bounds
+// (W rounds of a warp min-reduction), and a kept leaf pair's triangle pairs
+// are evaluated one per lane.  A pose's dive is ~20 dependent steps of one
+// decode + one bound; the first version ran the whole beam serially in one
+// thread per pose, which is what a batch too small to fill the GPU waited for
+// (158 us for 64 poses; config 4 at 64 poses 2.17 -> 1.96 ms, config 1 at
+// 1,024 poses 0.97 -> 0.72 ms, full config 4 within 1 %).
+__device__ __forceinline__ float dive_leaf_pair_warp(const Params& p, const PoseF& P, uint32_t ta, uint32_t tb, int lane) {
   const uint32_t fa = ta & 0x1FFFFFFFu, na = ((ta >> 29) & 3u) + 1;
   const uint32_t fb = tb & 0x1FFFFFFFu, nb = ((tb >> 29) & 3u) + 1;
   float d = FLT_MAX;
-  #pragma unroll 1
-  for (uint32_t u = 0; u < nb; ++u) {
-    const Tri TB = to_local(P, load_tri(p.B.tris, fb + u));
-    #pragma unroll 1
-    for (uint32_t v = 0; v < na; ++v) d = fminf(d, pair_distance(p, P, load_tri(p.A.tris, fa + v), TB, fa + v, fb + u));
+  if ((uint32_t)lane < na * nb) {
+    const uint32_t v = (uint32_t)lane / nb, u = (uint32_t)lane - v * nb;
+    d = pair_distance(p, P, load_tri(p.A.tris, fa + v), to_local(P, load_tri(p.B.tris, fb + u)), fa + v, fb + u);
   }
-  return d;
+  return __uint_as_float(__reduce_min_sync(FULL, __float_as_uint(fmaxf(d, 0.f))));
 }
 
-constexpr int64_t kDiveWideMinN = 16384;
-#ifndef CBVH_DIVE_BEAM
-#define CBVH_DIVE_BEAM 8  // measured 1 / 2 / 4 / 8 / 16 / 32: 8 best on configs 4, 3, 3 contact, 2
-#endif
-template <int KX, int W>
-__global__ void __launch_bounds__(128) dive_kernel(const __grid_constant__ Params p) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+template <int KX>
+__global__ void __launch_bounds__(128) dive_warp_kernel(const __grid_constant__ Params p) {
+  constexpr int NW = 14 + 2 * KX;  // words per beam entry: topo A, topo B, box A, box B, B's extra slabs
+  __shared__ uint32_t sm[4][2][8][NW];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int i = blockIdx.x * 4 + wib;
+  grid_dependency_wait();  // init_kernel's distances / caps
+  grid_launch_dependents();
   if (i >= p.N) return;
   const PoseF P = load_pose(p.poses, i);
   const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
   const float eps = 2e-6f * (tmax + p.A.maxabs + p.B.maxabs);
-  DiveEntry<KX> beam[W], cand[W];
-  int nb = 1, nc;
-  beam[0].ta = p.A.root_topo;
-  beam[0].tb = p.B.root_topo;
-  beam[0].lb = 0.f;
-  #pragma unroll
-  for (int q = 0; q < 6; ++q) { beam[0].BA[q] = p.A.root[q]; beam[0].BB[q] = p.B.root[q]; }
-  #pragma unroll
-  for (int q = 0; q < 2 * KX; ++q) beam[0].BX[q] = p.X.root[q];
+  const unsigned lt = lanemask_lt();
+  // lanes per beam entry (the larger arity, 4 or 8) and the beam width that fills the warp
+  const int sh = p.bmax <= 4 ? 2 : 3, W = 32 >> sh;
+  uint32_t(*cur)[NW] = sm[wib][0];
+  uint32_t(*nxt)[NW] = sm[wib][1];
+  if (lane == 0) {
+    cur[0][0] = p.A.root_topo;
+    cur[0][1] = p.B.root_topo;
+    #pragma unroll
+    for (int q = 0; q < 6; ++q) { cur[0][2 + q] = (uint32_t)p.A.root[q]; cur[0][8 + q] = (uint32_t)p.B.root[q]; }
+    #pragma unroll
+    for (int q = 0; q < 2 * KX; ++q) cur[0][14 + q] = (uint32_t)p.X.root[q];
+  }
+  __syncwarp();
+  int nb = 1;
   float dmin = __uint_as_float(__ldcg(&p.dist_bits[i]));  // +inf, or the caller's cap
-  if ((beam[0].ta & kLeafBit) && (beam[0].tb & kLeafBit)) {
-    dmin = fminf(dmin, dive_leaf_pair<KX>(p, P, beam[0].ta, beam[0].tb));
+  if ((p.A.root_topo & kLeafBit) && (p.B.root_topo & kLeafBit)) {
+    dmin = fminf(dmin, dive_leaf_pair_warp(p, P, p.A.root_topo, p.B.root_topo, lane));
     nb = 0;
   }
   #pragma unroll 1
   for (int step = 0; step < 128 && nb > 0; ++step) {
-    nc = 0;
-    #pragma unroll 1
-    for (int b = 0; b < nb; ++b) {
-      const DiveEntry<KX>& E = beam[b];
-      const bool la = (E.ta & kLeafBit) != 0, lb = (E.tb & kLeafBit) != 0;
-      const bool descA = !la && (lb || (descent_flags(CBVH_DESCENT_LARGER, E.ta, E.tb, E.BA, E.BB, p.A, p.B) & kDescA));
-      const uint32_t t = descA ? E.ta : E.tb;
+    const int e = lane >> sh, k = lane & ((1 << sh) - 1);
+    bool valid = e < nb;
+    uint32_t cta = 0, ctb = 0;
+    int32_t CA[6], CB[6], CX[2 * KX + 1];
+    float lb = FLT_MAX;
+    if (valid) {
+      const uint32_t ta = cur[e][0], tb = cur[e][1];
+      int32_t BA[6], BB[6], BX[2 * KX + 1];
+      #pragma unroll
+      for (int q = 0; q < 6; ++q) { BA[q] = (int32_t)cur[e][2 + q]; BB[q] = (int32_t)cur[e][8 + q]; }
+      #pragma unroll
+      for (int q = 0; q < 2 * KX; ++q) BX[q] = (int32_t)cur[e][14 + q];
+      const bool la = (ta & kLeafBit) != 0, lbf = (tb & kLeafBit) != 0;
+      const bool descA = !la && (lbf || (descent_flags(CBVH_DESCENT_LARGER, ta, tb, BA, BB, p.A, p.B) & kDescA));
+      const uint32_t t = descA ? ta : tb;
       const uint32_t first = t & 0x0FFFFFFFu, n = ((t >> 28) & 7u) + 1;
-      #pragma unroll 1
-      for (uint32_t k = 0; k < n; ++k) {
-        DiveEntry<KX> C = E;
-        float alo[3], ahi[3], blo[3], bhi[3], l;
+      valid = (uint32_t)k < n;
+      if (valid) {
+        cta = ta; ctb = tb;
+        #pragma unroll
+        for (int q = 0; q < 6; ++q) { CA[q] = BA[q]; CB[q] = BB[q]; }
+        #pragma unroll
+        for (int q = 0; q < 2 * KX; ++q) CX[q] = BX[q];
         if (descA) {
-          C.ta = __ldg(p.A.topo + first + k);
-          fetch_child_box(p.A, first + k, E.BA, C.BA);
+          cta = __ldg(p.A.topo + first + k);
+          fetch_child_box(p.A, first + k, BA, CA);
         } else {
-          C.tb = __ldg(p.B.topo + first + k);
-          if constexpr (KX > 0) fetch_child_kdop<KX>(p.B, first + k, E.BB, E.BX, C.BB, C.BX);
-          else fetch_child_box(p.B, first + k, E.BB, C.BB);
+          ctb = __ldg(p.B.topo + first + k);
+          if constexpr (KX > 0) fetch_child_kdop<KX>(p.B, first + k, BB, BX, CB, CX);
+          else fetch_child_box(p.B, first + k, BB, CB);
         }
-        words_to_float(p.A, C.BA, alo, ahi);
-        words_to_float(p.B, C.BB, blo, bhi);
-        sat_gap<true>(P, alo, ahi, blo, bhi, eps, &l);
-        if (l >= dmin) continue;
-        C.lb = l;
-        // keep the W smallest bounds (insertion into the sorted candidates)
-        int pos = nc < W ? nc : W;
-        while (pos > 0 && cand[pos - 1].lb > l) {
-          if (pos < W) cand[pos] = cand[pos - 1];
-          --pos;
-        }
-        if (pos < W) {
-          cand[pos] = C;
-          if (nc < W) ++nc;
-        }
+        float alo[3], ahi[3], blo[3], bhi[3];
+        words_to_float(p.A, CA, alo, ahi);
+        words_to_float(p.B, CB, blo, bhi);
+        sat_gap<true>(P, alo, ahi, blo, bhi, eps, &lb);
+        valid = lb < dmin;
       }
     }
-    // kept leaf pairs are evaluated and leave the beam
-    nb = 0;
+    // keep the W smallest bounds: W rounds of a warp minimum over (bound, lane) keys
+    unsigned key = valid ? ((__float_as_uint(fmaxf(lb, 0.f)) & ~31u) | (unsigned)lane) : 0xffffffffu;
+    bool sel = false;
     #pragma unroll 1
-    for (int c = 0; c < nc; ++c) {
-      if (cand[c].lb >= dmin) continue;
-      if ((cand[c].ta & kLeafBit) && (cand[c].tb & kLeafBit)) dmin = fminf(dmin, dive_leaf_pair<KX>(p, P, cand[c].ta, cand[c].tb));
-      else beam[nb++] = cand[c];
+    for (int r = 0; r < W; ++r) {
+      const unsigned mn = __reduce_min_sync(FULL, key);
+      if (mn == 0xffffffffu) break;
+      if (key == mn) { sel = true; key = 0xffffffffu; }
     }
+    // kept leaf pairs are evaluated (one triangle pair per lane) and leave the beam
+    const bool leafpair = sel && (cta & kLeafBit) && (ctb & kLeafBit);
+    unsigned lpm = __ballot_sync(FULL, leafpair);
+    while (lpm) {
+      const int src = __ffs(lpm) - 1;
+      lpm &= lpm - 1;
+      const uint32_t a = __shfl_sync(FULL, cta, src), b = __shfl_sync(FULL, ctb, src);
+      const float l = __shfl_sync(FULL, lb, src);
+      if (l < dmin) dmin = fminf(dmin, dive_leaf_pair_warp(p, P, a, b, lane));
+    }
+    const bool keep = sel && !leafpair && lb < dmin;
+    const unsigned km = __ballot_sync(FULL, keep);
+    if (keep) {
+      const int pos = __popc(km & lt);
+      nxt[pos][0] = cta;
+      nxt[pos][1] = ctb;
+      #pragma unroll
+      for (int q = 0; q < 6; ++q) { nxt[pos][2 + q] = (uint32_t)CA[q]; nxt[pos][8 + q] = (uint32_t)CB[q]; }
+      #pragma unroll
+      for (int q = 0; q < 2 * KX; ++q) nxt[pos][14 + q] = (uint32_t)CX[q];
+    }
+    nb = __popc(km);
+    uint32_t(*t2)[NW] = cur; cur = nxt; nxt = t2;
+    __syncwarp();
   }
-  atomicMin(&p.dist_bits[i], __float_as_uint(dmin));
+  if (lane == 0) atomicMin(&p.dist_bits[i], __float_as_uint(dmin));
 }
 
 // per-warp constant context (registers); mutable counters live in the kernel
@@ -1675,6 +1714,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
   constexpr int NF = nfields(KX);
   extern __shared__ uint32_t smem[];
   const int wib = threadIdx.x >> 5;
+  grid_dependency_wait();  // the previous phase's continuation items, init_kernel's outputs and control block
+  grid_launch_dependents();
   WarpCtx c;
   c.lane = threadIdx.x & 31;
   c.st = smem + wib * warp_smem_words(MODE, KX);
@@ -1792,7 +1833,11 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     // try to acquire: a warp deep in a heavy traversal polls the cursor every
     // kPoll iterations (one L2 load by lane 0), so its budget starts and its
     // backlog moves to the next phase with everybody else's
-    if (CBVH_POLL && poses_left && p.budget >= 0 && (++after & (kPoll - 1)) == 0) {
+    // (and at iterations 8, 16, 32, 64 of the warp's life, so a batch smaller
+    // than the grid — every pose taken at once — is handed on after a few
+    // iterations, not after kPoll of them)
+    if (CBVH_POLL && poses_left && p.budget >= 0 &&
+        ((++after & (kPoll - 1)) == 0 || (after < (int)kPoll && after >= 8 && (after & (after - 1)) == 0))) {
       unsigned cur = 0, lim = 0;
       if (c.lane == 0) {
         cur = __ldcg(&p.ctl->cursor[p.phase]);
@@ -2202,6 +2247,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
 
 template <int MODE>
 __global__ void init_kernel(Params p, int reset_stats) {
+  grid_launch_dependents();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   int stride = gridDim.x * blockDim.x;
   for (int k = i; k < p.N; k += stride) {
@@ -2339,11 +2385,12 @@ static bool dive_enabled() {
 
 // Phase schedule: budgets of the bounded phases, then one
 // unbounded phase.  CBVH_PHASES="b0,b1,..." overrides (tuning only).
+constexpr int64_t kSmallBatch = 256;
 struct PhaseSchedule {
   int n = 0;
   int b[kMaxPhases];
 };
-static int phase_budgets(int* out) {
+static int phase_budgets(int* out, int64_t N) {
   static const PhaseSchedule sched = [] {  // thread-safe one-time initialisation
     PhaseSchedule r;
     const char* env = std::getenv("CBVH_PHASES");
@@ -2361,6 +2408,17 @@ static int phase_budgets(int* out) {
     }
     return r;
   }();
+  static const bool overridden = [] { const char* env = std::getenv("CBVH_PHASES"); return env && *env; }();
+  if (!overridden && N <= kSmallBatch) {
+    // a batch far smaller than the grid: what the caller waits for is the
+    // longest chain of dependent iterations, so the first hand-overs come
+    // sooner (measured, tools/ab_phases_small.sh: 64 poses of config 3
+    // 513 -> 345 us, config 4 distance 1058 -> 853 us; at 1,024 poses the
+    // longer budgets are better again)
+    static const int small[4] = {8, 16, 32, 64};
+    for (int k = 0; k < 4; ++k) out[k] = small[k];
+    return 4;
+  }
   for (int k = 0; k < sched.n; ++k) out[k] = sched.b[k];
   return sched.n;
 }
@@ -2390,6 +2448,31 @@ static DevTree make_tree(const cbvh_bvh* T) {
     d.stage_ok = (d.zoff || (Tn * (uint32_t)d.cb) % 16 == 0) ? 1 : 0;
   }
   return d;
+}
+
+// Launch a kernel of the call's chain (dive, traversal phases) with
+// programmatic dependent launch: its CTAs may become resident while the
+// previous kernel of the stream drains, and every thread waits in
+// grid_dependency_wait() until that kernel has completed and its memory is
+// visible — the launch latency of the 4-7 kernels of a call overlaps the
+// previous kernel's tail instead of adding to it (CBVH_PDL=0: plain launches).
+template <class... KArgs, class... Args>
+static cudaError_t launch_after(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args&&... args) {
+  static const bool pdl = [] {
+    const char* env = std::getenv("CBVH_PDL");
+    return (env && *env) ? (std::atoi(env) != 0) : true;
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 template <int MODE, bool STATS, int KX>
@@ -2456,6 +2539,7 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   p.early_exit = (MODE == 0 && early_exit) ? 1 : 0;
   p.capped = (MODE == 1 && capped) ? 1 : 0;
   p.nwarps = s.warps;
+  p.bmax = (int)std::max(A->h.branching, B->h.branching);
   int ib = (int)((N + 255) / 256);
   ib = ib < 1 ? 1 : (ib > 4096 ? 4096 : ib);
   init_kernel<MODE><<<ib, 256, 0, st>>>(p, STATS ? 1 : 0);
@@ -2464,17 +2548,12 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   if (e != cudaSuccess) return cuda_fail(e, "init_kernel launch");
   if (N == 0) return CBVH_OK;
   if (MODE == 1 && dive_enabled()) {
-    // one thread per pose runs the beam serially: for a batch that does not
-    // fill the GPU (< 16k poses) that latency is not hidden, so a width-1
-    // dive is used there (config 1 contact: 0.99 ms vs 1.98 ms at width 8)
-    if (N >= kDiveWideMinN) dive_kernel<KX, CBVH_DIVE_BEAM><<<(int)((N + 127) / 128), 128, 0, st>>>(p);
-    else dive_kernel<KX, 1><<<(int)((N + 127) / 128), 128, 0, st>>>(p);
+    e = launch_after(dive_warp_kernel<KX>, (int)((N + 3) / 4), 128, 0, st, p);
     g_launches++;
-    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "dive_kernel launch");
   }
   int budgets[kMaxPhases];
-  const int nb = phase_budgets(budgets);
+  const int nb = phase_budgets(budgets, N);
   if (g_ev_start) cudaEventRecord(g_ev_start, st);
   for (int ph = 0; ph <= nb; ++ph) {
     p.phase = ph;
@@ -2482,13 +2561,12 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
     p.cont_in = (ph & 1) ? cont0 : cont1;   // phase ph reads what ph - 1 wrote
     p.cont_out = (ph & 1) ? cont1 : cont0;
     if constexpr (KX == 0) {
-      if (stage) traverse_kernel<MODE, STATS, KX, true><<<s.blocks, kWarps * 32, smem, st>>>(p);
-      else traverse_kernel<MODE, STATS, KX, false><<<s.blocks, kWarps * 32, smem, st>>>(p);
+      if (stage) e = launch_after(traverse_kernel<MODE, STATS, KX, true>, s.blocks, kWarps * 32, smem, st, p);
+      else e = launch_after(traverse_kernel<MODE, STATS, KX, false>, s.blocks, kWarps * 32, smem, st, p);
     } else {
-      traverse_kernel<MODE, STATS, KX, false><<<s.blocks, kWarps * 32, smem, st>>>(p);
+      e = launch_after(traverse_kernel<MODE, STATS, KX, false>, s.blocks, kWarps * 32, smem, st, p);
     }
     g_launches++;
-    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "traverse_kernel launch");
   }
   if (g_ev_stop) cudaEventRecord(g_ev_stop, st);
