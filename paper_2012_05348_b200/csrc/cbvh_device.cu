@@ -2086,13 +2086,14 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
 #if CBVH_DIST_FILTER
           // against a leaf: per-triangle bounds (masks for the leaf phase, and
           // a tighter pair bound)
-          if (surv && (ctb & kLeafBit)) {
+          const bool refine = CBVH_DIST_FILTER == 1 || ((cta & kLeafBit) && (ctb & kLeafBit));
+          if (surv && refine && (ctb & kLeafBit)) {
             float l2;
             mskB = box_near_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps, best, &l2, mskB);
             lb = fmaxf(lb, l2);
             surv = mskB != 0u;
           }
-          if (surv && (cta & kLeafBit)) {
+          if (surv && refine && (cta & kLeafBit)) {
             float l2;
             mskA = box_near_leaf<1>(P, blo, bhi, p.A.tris, cta, eps, best, &l2, mskA);
             lb = fmaxf(lb, l2);

@@ -731,3 +731,34 @@ def test_concurrent_streams_distinct_workspaces(M, cfg1):
         # (the visiting order may differ between runs; the minimum agrees to
         # fp32 rounding of near-tied candidates)
         assert np.allclose(d3.cpu().numpy(), ref_d, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("n", [1, 3, 64, 200, 257])
+def test_small_batches_short_schedule(M, cfg1, n):
+    # batches far below the grid size take the short phase schedule and the
+    # early cursor polls: counts match the band rule and the
+    # full batch's answers, distances the oracle's
+    w, tA, tB, delta, cnt, H, Z = cfg1
+    A, B = build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet)
+    # the heaviest poses first, so a tiny batch still has deep traversals to hand over
+    order = np.argsort(-(H + Z), kind="stable")[:n]
+    P = w.poses[order]
+    hit, gc = run_collide(M, A, B, P)
+    check_collide(hit, gc, H[order], Z[order], f"small batch {n}")
+    full_hit, full_gc = run_collide(M, A, B, w.poses)
+    assert np.array_equal(gc, full_gc[order]) and np.array_equal(hit, full_hit[order])
+    d64, _ = O.distance(tA, tB, P[:64])
+    g = run_distance(M, A, B, P[:64])
+    check_distance(g, d64, delta, f"small batch {n} distance")
+
+
+@pytest.mark.parametrize("Bf,kdop", [(8, 6), (2, 6), (8, 14), (4, 26)])
+def test_warp_dive_arities(M, cfg1, Bf, kdop):
+    # the warp dive gives a beam entry 4 or 8 lanes (the larger arity of the
+    # two trees) and carries B's k-DOP slabs: distances against the oracle for
+    # 8-ary and binary trees and k-DOP environments
+    w, tA, tB, delta = cfg1[:4]
+    A, B = build(M, w.A, Bf, 8), build(M, w.B, Bf, 8, kdop=kdop)
+    P = w.poses[:192]
+    d64, _ = O.distance(tA, tB, P)
+    check_distance(run_distance(M, A, B, P), d64, delta, f"warp dive B={Bf} k={kdop}")
