@@ -320,9 +320,9 @@ def run(args):
         w.branching = args.branching
     if args.bits:
         w.bits = args.bits
-    A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout,
+    A = M.build_compressed_bvh(w.A.vertices, w.A.triangles, w.branching, w.bits, w.treelet, args.leaf_a or w.leaf, args.layout,
                                align_treelets=args.align_treelets, zero_suppress=args.zero_suppress)
-    B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, w.leaf, args.layout,
+    B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet, args.leaf_b or w.leaf, args.layout,
                                kdop=args.kdop, align_treelets=args.align_treelets, zero_suppress=args.zero_suppress)
     distance = (w.mode if args.mode == "auto" else args.mode) == "distance"
     build_s = time.time() - t0
@@ -531,6 +531,8 @@ def main():
     ap.add_argument("--quick", action="store_true", help="timed steps only (A/B comparisons)")
     ap.add_argument("--branching", type=int, default=0, help="override B (config-3 sweep)")
     ap.add_argument("--leaf", type=int, default=0, help="override the leaf size c (1..4)")
+    ap.add_argument("--leaf-a", type=int, default=0, help="leaf size of the moving model A only (ablation)")
+    ap.add_argument("--leaf-b", type=int, default=0, help="leaf size of the static model B only (ablation)")
     ap.add_argument("--bits", type=int, default=0, help="override b (config-3 sweep)")
     ap.add_argument("--descent", default="larger", choices=["larger", "simultaneous"])
     ap.add_argument("--preset", default="random", choices=["random", "contact", "zero"],
