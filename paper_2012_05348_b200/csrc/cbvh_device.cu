@@ -203,8 +203,14 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 // ---------------------------------------------------------------- decode
 
+// FAST (template parameter of the decode helpers and of traverse_kernel): the
+// default blob format — delta layout, b = 8 in 8-bit fields, codes not
+// zero-suppressed — as compile-time constants, so the per-child format
+// branches (and their constant loads) disappear from the production kernel;
+// every other format takes the generic instantiation.
+template <bool FAST = false>
 __device__ __forceinline__ void load_codes(const DevTree& T, uint32_t node, uint32_t q[6]) {
-  if (T.width == 8) {
+  if (FAST || T.width == 8) {
     const unsigned short* p = reinterpret_cast<const unsigned short*>(T.codes + 6ull * node);
     uint32_t a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
     q[0] = a & 255u; q[1] = a >> 8; q[2] = b & 255u; q[3] = b >> 8; q[4] = c & 255u; q[5] = c >> 8;
@@ -289,18 +295,19 @@ __device__ __noinline__ uint3 load_codes_zs_global(const uint8_t* codes, const u
 // A node's box travels as 6 words: lattice ints (DELTA) or fp32 bits
 // (FP16 / FP32, absolute).  The child box comes from the parent's words
 // (DELTA: predictor-corrector decode) or straight from the record.
+template <bool FAST = false>
 __device__ __forceinline__ void fetch_child_box(const DevTree& T, uint32_t node, const int32_t P[6], int32_t C[6]) {
-  if (T.layout == CBVH_LAYOUT_DELTA) {
+  if (FAST || T.layout == CBVH_LAYOUT_DELTA) {
     uint32_t q[6];
     // (zero-suppressed blobs: an out-of-line call, so the common path keeps
     // its registers and code layout; CBVH_ZS=0 builds without the branch)
-    if (CBVH_ZS && T.zoff) {
+    if (!FAST && CBVH_ZS && T.zoff) {
       const uint3 z = load_codes_zs_global(T.codes, T.zoff, T.tlog, T.width, node);
       q[0] = z.x & 0xffffu; q[1] = z.x >> 16; q[2] = z.y & 0xffffu; q[3] = z.y >> 16; q[4] = z.z & 0xffffu; q[5] = z.z >> 16;
     } else {
-      load_codes(T, node, q);
+      load_codes<FAST>(T, node, q);
     }
-    decode_child(P, q, T.bits, C);
+    decode_child(P, q, FAST ? 8 : T.bits, C);
   } else if (T.layout == CBVH_LAYOUT_FP16) {
     // binary16 descriptors (§III.A): widened exactly to fp32
     const uint32_t* w = reinterpret_cast<const uint32_t*>(T.codes + 12ull * node);
@@ -316,8 +323,9 @@ __device__ __forceinline__ void fetch_child_box(const DevTree& T, uint32_t node,
   }
 }
 
+template <bool FAST = false>
 __device__ __forceinline__ void words_to_float(const DevTree& T, const int32_t C[6], float lo[3], float hi[3]) {
-  if (T.layout == CBVH_LAYOUT_DELTA) {
+  if (FAST || T.layout == CBVH_LAYOUT_DELTA) {
     to_float_box(T, C, lo, hi);
   } else {
     #pragma unroll
@@ -326,8 +334,9 @@ __device__ __forceinline__ void words_to_float(const DevTree& T, const int32_t C
 }
 
 // sum of the box's extents (the larger-first descent rule's size measure)
+template <bool FAST = false>
 __device__ __forceinline__ float words_extent(const DevTree& T, const int32_t C[6]) {
-  if (T.layout == CBVH_LAYOUT_DELTA)
+  if (FAST || T.layout == CBVH_LAYOUT_DELTA)
     return (float)((C[3] - C[0]) + (C[4] - C[1]) + (C[5] - C[2])) * T.cell;
   return (__int_as_float(C[3]) - __int_as_float(C[0])) + (__int_as_float(C[4]) - __int_as_float(C[1])) +
          (__int_as_float(C[5]) - __int_as_float(C[2]));
@@ -1069,11 +1078,12 @@ __device__ __forceinline__ int pair_count(uint32_t pw, uint32_t ta, uint32_t tb)
 // both when both are internal; the LARGER rule descends only the node with the
 // larger box (sum of extents, A-local vs world — rotation-invariant up to
 // sqrt 3), which visits the same leaf pairs (reading R15).
+template <bool FAST = false>
 __device__ __forceinline__ uint32_t descent_flags(int rule, uint32_t ta, uint32_t tb, const int32_t CA[6],
                                                   const int32_t CB[6], const DevTree& TA, const DevTree& TB) {
   const bool ai = !(ta & kLeafBit), bi = !(tb & kLeafBit);
   if (!(ai && bi) || rule == 0) return (ai ? kDescA : 0u) | (bi ? kDescB : 0u);
-  const float ea = words_extent(TA, CA), eb = words_extent(TB, CB);
+  const float ea = words_extent<FAST>(TA, CA), eb = words_extent<FAST>(TB, CB);
   return ea >= eb ? kDescA : kDescB;
 }
 
@@ -1477,7 +1487,7 @@ __device__ __forceinline__ void exact_batch(const Params& p, const WarpCtx c, in
 // expensive tests 32 at a time, so Möller / the distance code run with full
 // lanes instead of the ~20-30 % the culls leave.  Returns the number of
 // triangle-pair tests (stats).
-template <int MODE, bool STATS>
+template <int MODE, bool STATS, bool FAST = false>
 __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx c, int nleaf,
                                                  unsigned long long* exact) {
   unsigned tests = 0;
@@ -1494,7 +1504,7 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
       mk = c.lq[3 * kLeafQ + head + c.lane];
       n = (int)((mk >> 8) & 7u) * (int)((mk >> 19) & 7u);  // only triangles the box filters kept
       // early exit: a pose that already has a hit needs no more tests
-      if (MODE == 0 && p.early_exit && __ldcg(&p.hit[pose])) n = 0;
+      if (MODE == 0 && !FAST && p.early_exit && __ldcg(&p.hit[pose])) n = 0;
       // distance: a leaf pair whose box bound no longer beats the pose's best
       // distance (tightened since it was queued) is skipped
       if (MODE == 1 && __uint_as_float(c.lq[4 * kLeafQ + head + c.lane]) >= __uint_as_float(__ldcg(&p.dist_bits[pose])))
@@ -1709,13 +1719,16 @@ __host__ __device__ constexpr int min_blocks(int mode, int kx) {
   return kx == 0 ? (mode == 0 ? CBVH_MIN_BLOCKS : CBVH_MIN_BLOCKS_DIST) : (mode == 0 ? (kx >= 10 ? 3 : 4) : 3);
 }
 
-template <int MODE, bool STATS, int KX, bool STAGE>
+template <int MODE, bool STATS, int KX, bool STAGE, bool FAST>
 __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_kernel(const __grid_constant__ Params p) {
   constexpr int NF = nfields(KX);
   extern __shared__ uint32_t smem[];
   const int wib = threadIdx.x >> 5;
   grid_dependency_wait();  // the previous phase's continuation items, init_kernel's outputs and control block
   grid_launch_dependents();
+  static_assert(!FAST || (!STATS && KX == 0 && !STAGE), "FAST is the default-format production kernel");
+  const int early_exit = FAST ? 0 : p.early_exit;
+  const int descent = FAST ? CBVH_DESCENT_LARGER : p.descent;
   WarpCtx c;
   c.lane = threadIdx.x & 31;
   c.st = smem + wib * warp_smem_words(MODE, KX);
@@ -1779,7 +1792,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
             } else {
               const int slot = top + c.lane;
               c.st[F_POSE * kStack + slot] =
-                  (base + c.lane) | descent_flags(p.descent, p.A.root_topo, p.B.root_topo, p.A.root, p.B.root,
+                  (base + c.lane) | descent_flags<FAST>(descent, p.A.root_topo, p.B.root_topo, p.A.root, p.B.root,
                                                   p.A, p.B);
               c.st[F_TA * kStack + slot] = p.A.root_topo;
               c.st[F_TB * kStack + slot] = p.B.root_topo;
@@ -1796,7 +1809,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
           if (root_leafpair) nleaf += k; else top += k;
           __syncwarp();
           if (nleaf > kLeafQ - 32) {
-            s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
+            s_tri += drain_leaves<MODE, STATS, FAST>(p, c, nleaf, &s_exact);
             nleaf = 0;
           }
         }
@@ -1852,7 +1865,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     // ---- bounded work after the input ran out: hand the rest to the next phase
     if (!poses_left && p.budget >= 0 && ++after > p.budget) {
       if (nleaf > 0) {
-        s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
+        s_tri += drain_leaves<MODE, STATS, FAST>(p, c, nleaf, &s_exact);
         nleaf = 0;
       }
       if (dump_items<NF>(p, c, top, spill_top)) {
@@ -1879,7 +1892,9 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     const int n0 = __shfl_sync(FULL, n, 0);
     int m, total, passes;
     unsigned starts;
-    if (n0 > 32) {  // B = 8, both internal: one item in two passes
+    // (FAST descends one side per item — the larger-first rule — so an item
+    // has at most 8 child pairs and never needs a second pass)
+    if (!FAST && n0 > 32) {  // B = 8, both internal: one item in two passes
       m = 1; total = n0; passes = (n0 + 31) >> 5; starts = 1u;
 #if CBVH_LATE_LOADS
       // the item stays on the stack during its passes (its boxes are read
@@ -1930,7 +1945,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
     const float tmax = fmaxf(fabsf(P.t[0]), fmaxf(fabsf(P.t[1]), fabsf(P.t[2])));
     const float eps = 2e-6f * (tmax + scale_ab);
 #endif
-    const bool early_done = MODE == 0 && p.early_exit && __ldcg(&p.hit[pose]) != 0;
+    const bool early_done = MODE == 0 && early_exit && __ldcg(&p.hit[pose]) != 0;
     float best = FLT_MAX;
     if (MODE == 1) best = __uint_as_float(__ldcg(&p.dist_bits[pose]));
     const bool a_int = (pword & kDescA) != 0, b_int = (pword & kDescB) != 0;  // sides descended
@@ -1940,8 +1955,10 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       const int k = c.lane - start_e + 32 * pass;
       bool valid = (c.lane + 32 * pass) < total;
       if (MODE == 1) valid = valid && item_lb < best;
-      if (MODE == 0 && p.early_exit) valid = valid && !early_done;
-      const int i = small_div(k, nb), j = k - i * nb;
+      if (MODE == 0 && early_exit) valid = valid && !early_done;
+      // child indices on the two sides; with one side descended (FAST) the
+      // pair index is the child index of that side
+      const int i = FAST ? (b_int ? 0 : k) : small_div(k, nb), j = FAST ? (b_int ? k : 0) : k - i * nb;
       int32_t CA[6], CB[6], CX[2 * KX + 1];
       uint32_t cta = ta, ctb = tb;
       float sg = 0.f;  // collide: the SAT gap (early-exit push order)
@@ -1997,7 +2014,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
           if (STAGE) cta = fetch_child(c, p, p.A, slotA, node, BA, CA);
           else {
             cta = __ldg(p.A.topo + node);
-            fetch_child_box(p.A, node, BA, CA);
+            fetch_child_box<FAST>(p.A, node, BA, CA);
           }
         } else {
           #pragma unroll
@@ -2013,7 +2030,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
             ctb = fetch_child(c, p, p.B, slotB, node, BB, CB);
           } else {
             ctb = __ldg(p.B.topo + node);
-            fetch_child_box(p.B, node, BB, CB);
+            fetch_child_box<FAST>(p.B, node, BB, CB);
           }
         } else {
           #pragma unroll
@@ -2022,8 +2039,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
           for (int r = 0; r < 2 * KX; ++r) CX[r] = BX[r];
         }
         float alo[3], ahi[3], blo[3], bhi[3];
-        words_to_float(p.A, CA, alo, ahi);
-        words_to_float(p.B, CB, blo, bhi);
+        words_to_float<FAST>(p.A, CA, alo, ahi);
+        words_to_float<FAST>(p.B, CB, blo, bhi);
         if (smem_boxes(MODE)) {
           // park the child boxes in shared memory across the tests: under
           // register pressure the compiler spills them to local memory
@@ -2065,7 +2082,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
           if (la && lbf) {
             if (CBVH_PAIR_AFILTER == 0) doA = false;
             else if (CBVH_PAIR_AFILTER == 2)
-              doA = words_extent(p.B, CB) < CBVH_PAIR_RATIO * words_extent(p.A, CA);
+              doA = words_extent<FAST>(p.B, CB) < CBVH_PAIR_RATIO * words_extent<FAST>(p.A, CA);
           }
           const bool doB = lbf;
 #endif
@@ -2132,7 +2149,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
           else if (c.lane == last) pos = __popc(pm & ((1u << wl) - 1u));
         }
 #if CBVH_EE_ORDER
-        if (MODE == 0 && p.early_exit) {
+        if (MODE == 0 && early_exit) {
           // early exit: the deepest-overlapping pair (most negative SAT gap)
           // goes on top, to reach a first hit sooner
           const unsigned b = __float_as_uint(sg);
@@ -2154,7 +2171,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
               CB[q] = (int32_t)c.scr[(6 + q) * 32 + c.lane];
             }
           }
-          c.st[F_POSE * kStack + s2] = pose | descent_flags(p.descent, cta, ctb, CA, CB, p.A, p.B);
+          c.st[F_POSE * kStack + s2] = pose | descent_flags<FAST>(descent, cta, ctb, CA, CB, p.A, p.B);
           c.st[F_TA * kStack + s2] = cta;
           c.st[F_TB * kStack + s2] = ctb;
           #pragma unroll
@@ -2192,8 +2209,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       // CBVH_DIST_DRAIN: a sooner drain tightens a pose's best earlier, but
       // the half-empty rounds cost more than the pruning gains)
       if (nleaf > kLeafQ - 32 || (MODE == 1 && nleaf >= CBVH_DIST_DRAIN) ||
-          (MODE == 0 && p.early_exit && nleaf >= CBVH_EE_DRAIN)) {
-        s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
+          (MODE == 0 && early_exit && nleaf >= CBVH_EE_DRAIN)) {
+        s_tri += drain_leaves<MODE, STATS, FAST>(p, c, nleaf, &s_exact);
         nleaf = 0;
       }
     }
@@ -2205,11 +2222,11 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       top -= 1;
     }
     if (MODE == 1 && nleaf > 0 && top == 0) {
-      s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
+      s_tri += drain_leaves<MODE, STATS, FAST>(p, c, nleaf, &s_exact);
       nleaf = 0;
     }
   }
-  if (nleaf > 0) s_tri += drain_leaves<MODE, STATS>(p, c, nleaf, &s_exact);
+  if (nleaf > 0) s_tri += drain_leaves<MODE, STATS, FAST>(p, c, nleaf, &s_exact);
   if (STATS && c.lane == 0) atomicMax(&p.ctl->t_end, globaltimer_ns());
   if (STATS) {
     unsigned long long d = s_dec, r = s_rec, lb = s_lbytes, ex = s_exact;
@@ -2311,7 +2328,7 @@ constexpr int kMaxDevices = 64;
 
 // Grid of the persistent traversal kernel: SMs x resident CTAs at `smem`
 // bytes of dynamic shared memory per CTA.
-template <int MODE, bool STATS, int KX, bool STAGE>
+template <int MODE, bool STATS, int KX, bool STAGE, bool FAST = false>
 static int shape_for(LaunchShape* s, size_t smem) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -2329,10 +2346,10 @@ static int shape_for(LaunchShape* s, size_t smem) {
     e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
     if (smem > (size_t)optin) return set_error(CBVH_EINVAL, "shared memory of the staged kernel exceeds the device limit");
-    e = cudaFuncSetAttribute(traverse_kernel<MODE, STATS, KX, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(traverse_kernel<MODE, STATS, KX, STAGE, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              STAGE ? optin : (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel<MODE, STATS, KX, STAGE>, kWarps * 32,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel<MODE, STATS, KX, STAGE, FAST>, kWarps * 32,
                                                       smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
@@ -2353,7 +2370,14 @@ static int max_warps_kx(int mode) {
   if (rc) return -1;
   rc = mode == 0 ? shape_for<0, true, KX, false>(&b, smem_bytes(0, KX)) : shape_for<1, true, KX, false>(&b, smem_bytes(1, KX));
   if (rc) return -1;
-  return a.warps > b.warps ? a.warps : b.warps;
+  int w = a.warps > b.warps ? a.warps : b.warps;
+  if constexpr (KX == 0) {
+    LaunchShape f{};
+    rc = mode == 0 ? shape_for<0, false, 0, false, true>(&f, smem_bytes(0, 0)) : shape_for<1, false, 0, false, true>(&f, smem_bytes(1, 0));
+    if (rc) return -1;
+    w = f.warps > w ? f.warps : w;
+  }
+  return w;
 }
 
 static int max_warps(int mode, int kx) {
@@ -2379,6 +2403,15 @@ static int extra_axes(const cbvh_bvh* B) { return B ? (int)B->h.kdop / 2 - 3 : 0
 static bool dive_enabled() {
   static const bool on = [] {  // thread-safe one-time initialisation
     const char* env = std::getenv("CBVH_DIVE");
+    return (env && *env) ? (std::atoi(env) != 0) : true;
+  }();
+  return on;
+}
+
+// CBVH_FAST=0 sends the default format through the generic kernel too (A/B only)
+static bool fast_enabled() {
+  static const bool on = [] {
+    const char* env = std::getenv("CBVH_FAST");
     return (env && *env) ? (std::atoi(env) != 0) : true;
   }();
   return on;
@@ -2507,10 +2540,21 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
     if (stage && T->stage_ok) p.stage_slot_words = std::max(p.stage_slot_words, slot_words(*T));
   const size_t smem = smem_bytes(MODE, KX) +
                       (stage ? (size_t)kWarps * (kStageTagWords + kStageSlots * p.stage_slot_words) * sizeof(uint32_t) : 0);
+  // the default blob format and query options run the FAST instantiation
+  // (format constants folded at compile time); everything else the generic one
+  auto plain = [](const DevTree& T) { return T.layout == CBVH_LAYOUT_DELTA && T.width == 8 && T.bits == 8 && !T.zoff; };
+  const bool fast = !STATS && KX == 0 && !stage && plain(p.A) && plain(p.B) && descent == CBVH_DESCENT_LARGER &&
+                    !(MODE == 0 && early_exit) && fast_enabled();
   LaunchShape s;
   int rc;
-  if constexpr (KX == 0) rc = stage ? shape_for<MODE, STATS, KX, true>(&s, smem) : shape_for<MODE, STATS, KX, false>(&s, smem);
-  else rc = shape_for<MODE, STATS, KX, false>(&s, smem);
+  if constexpr (KX == 0 && !STATS) {
+    rc = stage ? shape_for<MODE, STATS, KX, true>(&s, smem)
+               : (fast ? shape_for<MODE, STATS, KX, false, true>(&s, smem) : shape_for<MODE, STATS, KX, false>(&s, smem));
+  } else if constexpr (KX == 0) {
+    rc = stage ? shape_for<MODE, STATS, KX, true>(&s, smem) : shape_for<MODE, STATS, KX, false>(&s, smem);
+  } else {
+    rc = shape_for<MODE, STATS, KX, false>(&s, smem);
+  }
   if (rc) return rc;
   if (ws_bytes < workspace_for_warps(s.warps, KX)) return set_error(CBVH_EWORKSPACE, "workspace too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -2561,11 +2605,15 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
     p.budget = ph < nb ? budgets[ph] : -1;
     p.cont_in = (ph & 1) ? cont0 : cont1;   // phase ph reads what ph - 1 wrote
     p.cont_out = (ph & 1) ? cont1 : cont0;
-    if constexpr (KX == 0) {
-      if (stage) e = launch_after(traverse_kernel<MODE, STATS, KX, true>, s.blocks, kWarps * 32, smem, st, p);
-      else e = launch_after(traverse_kernel<MODE, STATS, KX, false>, s.blocks, kWarps * 32, smem, st, p);
+    if constexpr (KX == 0 && !STATS) {
+      if (stage) e = launch_after(traverse_kernel<MODE, STATS, KX, true, false>, s.blocks, kWarps * 32, smem, st, p);
+      else if (fast) e = launch_after(traverse_kernel<MODE, STATS, KX, false, true>, s.blocks, kWarps * 32, smem, st, p);
+      else e = launch_after(traverse_kernel<MODE, STATS, KX, false, false>, s.blocks, kWarps * 32, smem, st, p);
+    } else if constexpr (KX == 0) {
+      if (stage) e = launch_after(traverse_kernel<MODE, STATS, KX, true, false>, s.blocks, kWarps * 32, smem, st, p);
+      else e = launch_after(traverse_kernel<MODE, STATS, KX, false, false>, s.blocks, kWarps * 32, smem, st, p);
     } else {
-      e = launch_after(traverse_kernel<MODE, STATS, KX, false>, s.blocks, kWarps * 32, smem, st, p);
+      e = launch_after(traverse_kernel<MODE, STATS, KX, false, false>, s.blocks, kWarps * 32, smem, st, p);
     }
     g_launches++;
     if (e != cudaSuccess) return cuda_fail(e, "traverse_kernel launch");

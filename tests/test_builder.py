@@ -567,6 +567,7 @@ def test_production_kernels_do_not_spill(tmp_path):
                          capture_output=True, text=True, check=True).stderr
     lines = out.splitlines()
     for mode in (0, 1):
-        tag = f"_ZN4cbvh15traverse_kernelILi{mode}ELb0ELi0ELb0EEEvNS_6ParamsE"
-        i = next(k for k, l in enumerate(lines) if "Function properties for " + tag in l)
-        assert "0 bytes spill stores, 0 bytes spill loads" in lines[i + 1], lines[i + 1]
+        for fast in (0, 1):  # the generic and the default-format (FAST) instantiations
+            tag = f"_ZN4cbvh15traverse_kernelILi{mode}ELb0ELi0ELb0ELb{fast}EEEvNS_6ParamsE"
+            i = next(k for k, l in enumerate(lines) if "Function properties for " + tag in l)
+            assert "0 bytes spill stores, 0 bytes spill loads" in lines[i + 1], lines[i + 1]
