@@ -195,6 +195,29 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 __device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Inclusive warp prefix sum: shfl.up's in-range predicate guards the add, so a
+// step is two instructions (the intrinsic form compiles to a shuffle, a lane
+// compare, a select and an add).
+#ifndef CBVH_ASM_SCAN
+#define CBVH_ASM_SCAN 1
+#endif
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#if CBVH_ASM_SCAN
+  (void)lane;
+  #pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+    asm volatile("{ .reg .s32 r; .reg .pred q; shfl.sync.up.b32 r|q, %0, %1, 0, 0xffffffff; @q add.s32 %0, %0, r; }"
+                 : "+r"(v) : "r"(o));
+#else
+  #pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+#endif
+  return v;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -606,6 +629,9 @@ __device__ __forceinline__ bool tri_boxes_overlap(const Tri& V, const Tri& U) {
 #ifndef CBVH_PAIR_RATIO
 #define CBVH_PAIR_RATIO 1.5f  // measured: config 5 -4.5 %, configs 3 / 2 +1 / +2 % (always: config 3 -3.5 %; never: config 5 +6 %)
 #endif
+// (The early return after the box axes stays: straight-line code without it
+// measured 1 % slower on config 5 and 3 % on config 3 — whole warps do leave
+// here.  The same for Möller's plane rejections: neutral.)
 template <int AXES>
 __device__ __forceinline__ bool box_tri_overlap(const float c[3], const float h[3], const Tri& T, float eps) {
   float v[3][3];
@@ -1062,8 +1088,12 @@ __device__ __noinline__ float tri_dist_fp64(const PoseF& P, const float* trisA, 
 __host__ __device__ constexpr bool smem_boxes(int mode) { return (CBVH_SMEM_BOXES >> mode) & 1; }
 constexpr int kSurv = 64;  // exact-test queue entries per warp (pose, tri A, tri B)
 // per-warp shared memory: stack + leaf queue (+ the exact-test queue, distance only)
+#ifndef CBVH_PACK_LUT
+#define CBVH_PACK_LUT 1  // pack_list of a 4-bit mask from a 16-word per-warp table (one LDS instead of ~17 ALU operations)
+#endif
 __host__ __device__ constexpr int warp_smem_words(int mode, int kx) {
-  return nfields(kx) * kStack + 5 * kLeafQ + (mode == 1 ? 3 * kSurv : 0) + (smem_boxes(mode) ? 12 * 32 : 0);
+  return nfields(kx) * kStack + 5 * kLeafQ + (mode == 1 ? 3 * kSurv : 0) + (smem_boxes(mode) ? 12 * 32 : 0) +
+         (CBVH_PACK_LUT ? 16 : 0);
 }
 
 // child pairs of an item: Alg. 1 enumerates children of every side it
@@ -1254,6 +1284,7 @@ struct WarpCtx {
   uint32_t* lq;     // leaf queue SoA [5][kLeafQ]: pose, topoA, topoB, triangle lists, lower bound (distance)
   uint32_t* sq;     // exact-test queue SoA [3][kSurv]: pose, triangle of A, triangle of B
   uint32_t* scr;    // per-lane parking of the child boxes [12][32] (CBVH_SMEM_BOXES)
+  uint32_t* lut;    // pack_list of every 4-bit mask [16] (CBVH_PACK_LUT)
   uint32_t* spill;  // this warp's global spill area [kSpillCap][nfields(KX)]
   uint32_t* stag;   // staging: slot tags [kStageSlots] (tree bit | block id; kNoBlock = empty)
   uint32_t* stg;    // staging: slots [kStageSlots][stage_slot_words]
@@ -1510,12 +1541,7 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
       if (MODE == 1 && __uint_as_float(c.lq[4 * kLeafQ + head + c.lane]) >= __uint_as_float(__ldcg(&p.dist_bits[pose])))
         n = 0;
     }
-    int incl = n;
-    #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(FULL, incl, o);
-      if (c.lane >= o) incl += y;
-    }
+    const int incl = warp_incl_scan(n, c.lane);
     const unsigned fit = __ballot_sync(FULL, c.lane < avail && incl <= 32);
     const int m = __popc(fit);  // >= 2: an entry has at most 16 triangle pairs
     const int total = __shfl_sync(FULL, incl, m - 1);
@@ -1715,12 +1741,22 @@ __device__ __noinline__ bool dump_items(const Params& p, const WarpCtx c, int to
 
 // resident CTAs per SM the register allocation targets (k-DOP stacks take
 // more shared memory and registers)
-__host__ __device__ constexpr int min_blocks(int mode, int kx) {
-  return kx == 0 ? (mode == 0 ? CBVH_MIN_BLOCKS : CBVH_MIN_BLOCKS_DIST) : (mode == 0 ? (kx >= 10 ? 3 : 4) : 3);
+// The FAST collide instantiation needs fewer registers (80 at 6 CTAs / SM
+// without a spill, 72 at 7 with 16 bytes of them), so more warps hide the
+// latencies of this issue-bound kernel: measured 5 / 6 / 7 / 8 CTAs per SM
+// (8 with a 80-entry stack to fit shared memory): config 5 40.1 / 38.1 /
+// 37.3 / 38.0 ms, config 3 45.4 / 42.8 / 42.0 / 42.7, config 2 3.44 / 3.46 /
+// 3.55 / 3.94 (profiles/round2_ab_occupancy.txt).
+#ifndef CBVH_MIN_BLOCKS_FAST
+#define CBVH_MIN_BLOCKS_FAST 7
+#endif
+__host__ __device__ constexpr int min_blocks(int mode, int kx, bool fast = false) {
+  return kx == 0 ? (mode == 0 ? (fast ? CBVH_MIN_BLOCKS_FAST : CBVH_MIN_BLOCKS) : CBVH_MIN_BLOCKS_DIST)
+                 : (mode == 0 ? (kx >= 10 ? 3 : 4) : 3);
 }
 
 template <int MODE, bool STATS, int KX, bool STAGE, bool FAST>
-__global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) traverse_kernel(const __grid_constant__ Params p) {
   constexpr int NF = nfields(KX);
   extern __shared__ uint32_t smem[];
   const int wib = threadIdx.x >> 5;
@@ -1735,6 +1771,11 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
   c.lq = c.st + NF * kStack;
   c.sq = c.lq + 5 * kLeafQ;
   c.scr = c.sq + (MODE == 1 ? 3 * kSurv : 0);
+  c.lut = c.scr + (smem_boxes(MODE) ? 12 * 32 : 0);
+  if (CBVH_PACK_LUT) {
+    if (c.lane < 16) c.lut[c.lane] = pack_list((uint32_t)c.lane);
+    __syncwarp();
+  }
   c.spill = p.spill + (size_t)(blockIdx.x * kWarps + wib) * kSpillCap * NF;
   // staging area after all warps' stacks and queues
   c.stag = smem + kWarps * warp_smem_words(MODE, KX) + wib * (kStageTagWords + kStageSlots * p.stage_slot_words);
@@ -1883,12 +1924,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
       const int slot = top - 1 - c.lane;
       n = pair_count(c.st[F_POSE * kStack + slot], c.st[F_TA * kStack + slot], c.st[F_TB * kStack + slot]);
     }
-    int incl = n;
-    #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(FULL, incl, o);
-      if (c.lane >= o) incl += y;
-    }
+    const int incl = warp_incl_scan(n, c.lane);
     const int n0 = __shfl_sync(FULL, n, 0);
     int m, total, passes;
     unsigned starts;
@@ -2195,7 +2231,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX)) traverse_ke
           c.lq[0 * kLeafQ + s2] = pose;
           c.lq[1 * kLeafQ + s2] = cta;
           c.lq[2 * kLeafQ + s2] = ctb;
-          c.lq[3 * kLeafQ + s2] = pack_list(mskA & full_mask(cta)) | (pack_list(mskB & full_mask(ctb)) << 11);
+          c.lq[3 * kLeafQ + s2] = CBVH_PACK_LUT ? (c.lut[mskA & full_mask(cta)] | (c.lut[mskB & full_mask(ctb)] << 11))
+                                                : (pack_list(mskA & full_mask(cta)) | (pack_list(mskB & full_mask(ctb)) << 11));
           if (MODE == 1) c.lq[4 * kLeafQ + s2] = __float_as_uint(lb);
         }
         nleaf += __popc(lm);

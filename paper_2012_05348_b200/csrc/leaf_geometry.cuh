@@ -97,12 +97,13 @@ template <class F>
 __device__ __forceinline__ bool interval(const F p[3], const F d[3], F* t0, F* t1) {
 #if CBVH_MOLLER_SELECT
   // the same case analysis as below, as selects (no divergent branches)
+  // (bitwise operators on the flags: no short-circuit branches)
   const bool c1 = d[0] * d[1] > 0;
-  const bool c2 = !c1 && d[0] * d[2] > 0;
-  const bool c3 = !c1 && !c2 && (d[1] * d[2] > 0 || d[0] != 0);
-  const bool c4 = !c1 && !c2 && !c3 && d[1] != 0;
-  const bool c5 = !c1 && !c2 && !c3 && !c4 && d[2] != 0;
-  const bool k2 = c1 || c5, k1 = c2 || c4;  // else k = 0 (c3)
+  const bool c2 = !c1 & (d[0] * d[2] > 0);
+  const bool c3 = !c1 & !c2 & ((d[1] * d[2] > 0) | (d[0] != 0));
+  const bool c4 = !c1 & !c2 & !c3 & (d[1] != 0);
+  const bool c5 = !c1 & !c2 & !c3 & !c4 & (d[2] != 0);
+  const bool k2 = c1 | c5, k1 = c2 | c4;  // else k = 0 (c3)
   const F pk = k2 ? p[2] : (k1 ? p[1] : p[0]), dk = k2 ? d[2] : (k1 ? d[1] : d[0]);
   const F pi = c3 ? p[1] : p[0], di = c3 ? d[1] : d[0];
   const F pj = k2 ? p[1] : p[2], dj = k2 ? d[1] : d[2];
@@ -110,7 +111,7 @@ __device__ __forceinline__ bool interval(const F p[3], const F d[3], F* t0, F* t
   const F b = pk + (pj - pk) * div_(dk, dk - dj);
   *t0 = fmin(a, b);
   *t1 = fmax(a, b);
-  return c1 || c2 || c3 || c4 || c5;
+  return c1 | c2 | c3 | c4 | c5;
 #else
   int k, i, j;
   if (d[0] * d[1] > 0) { k = 2; i = 0; j = 1; }

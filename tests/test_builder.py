@@ -570,4 +570,11 @@ def test_production_kernels_do_not_spill(tmp_path):
         for fast in (0, 1):  # the generic and the default-format (FAST) instantiations
             tag = f"_ZN4cbvh15traverse_kernelILi{mode}ELb0ELi0ELb0ELb{fast}EEEvNS_6ParamsE"
             i = next(k for k, l in enumerate(lines) if "Function properties for " + tag in l)
-            assert "0 bytes spill stores, 0 bytes spill loads" in lines[i + 1], lines[i + 1]
+            if (mode, fast) == (0, 1):
+                # the default-format collide kernel runs 7 CTAs / SM at 72 registers:
+                # at most a few bytes of spills (measured faster than 6 CTAs without any)
+                import re
+                st, ld = map(int, re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", lines[i + 1]).groups())
+                assert st <= 32 and ld <= 32, lines[i + 1]
+            else:
+                assert "0 bytes spill stores, 0 bytes spill loads" in lines[i + 1], lines[i + 1]
