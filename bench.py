@@ -129,6 +129,17 @@ def aggregate_rate(units_per_rank: int, steps: int, world: int, seconds: float) 
     return units_per_rank * steps * world / seconds
 
 
+def kernel_source_sha() -> str:
+    """Hash of the kernel sources (tools/launch_totals.py stores the same hash
+    with the ncu instruction counts it commits)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("cbvh_device.cu", "leaf_geometry.cuh"):
+        with open(os.path.join(ROOT, "paper_2012_05348_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -426,6 +437,8 @@ def run(args):
     # against 148 SMs x 4 schedulers x the max SM clock
     issue = None
     winst = nc.get("warp_inst_per_launch") if not distance and args.layout == "delta" and args.kdop == 6 else None
+    if winst and nc.get("kernel_source_sha256") != kernel_source_sha():
+        winst = None  # the committed instruction count belongs to other kernel sources: not reported
     if winst:
         ipeak = 148 * 4 * peaks.get("sm_max_mhz", 1965.0) * 1e6
         issue = {"bound": "issue", "achieved": winst / kern_s, "peak": ipeak, "unit": "warp inst/s",

@@ -4,8 +4,10 @@ written into profiles/ncu_traffic.json next to the DRAM bytes of the full captur
 
 usage: python tools/launch_totals.py launches.csv cfg5 [phases_per_call=4] [source-name]"""
 import csv
+import hashlib
 import json
 import os
+import re
 import sys
 from collections import defaultdict
 
@@ -16,8 +18,8 @@ rows = [r for r in csv.reader(open(path)) if len(r) > 14 and r[0].isdigit()]
 per = defaultdict(lambda: defaultdict(float))
 for r in rows:
     kid, name, metric, val = r[0], r[4], r[12], r[14]
-    if any(t in name for t in ("traverse_kernel<0, 0, 0>", "traverse_kernel<0, false, 0>",
-                               "traverse_kernel<0, false, 0, false>", "traverse_kernel<0, 0, 0, 0>")):
+    # the production collide instantiations: MODE 0, STATS off, AABB blobs (any STAGE / FAST)
+    if re.search(r"traverse_kernel<\(?(int\))?0, \(?(bool\))?(0|false), \(?(int\))?0[,>]", name):
         per[kid][metric] = float(val.replace(",", ""))
 n = len(per)
 tot = defaultdict(float)
@@ -32,6 +34,13 @@ out = {"warp_inst_per_launch": tot["smsp__inst_executed.sum"] / calls,
 print(json.dumps(out))
 p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "ncu_traffic.json")
 d = json.load(open(p)) if os.path.exists(p) else {}
+# the kernel sources these counts belong to: bench.py reports roofline_issue
+# only while the committed counts match the sources it runs
+csrc = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2012_05348_b200", "csrc")
+h = hashlib.sha256()
+for f in ("cbvh_device.cu", "leaf_geometry.cuh"):
+    h.update(open(os.path.join(csrc, f), "rb").read())
+out["kernel_source_sha256"] = h.hexdigest()
 d.setdefault(key, {}).update(out)
 d[key]["inst_source"] = (f"ncu launch list ({src}): smsp__inst_executed.sum and "
                          "smsp__thread_inst_executed.sum summed over the phases of each production collide call")
