@@ -429,7 +429,9 @@ def run(args):
         try:
             with open(prof) as f:
                 nc = json.load(f).get(f"cfg{args.config}", {})
-            traffic = nc.get("dram_bytes_per_launch")
+            # (the committed capture describes the kernel sources whose hash it
+            # stores: after a kernel change it is not reported until re-captured)
+            traffic = nc.get("dram_bytes_per_launch") if nc.get("kernel_source_sha256") == kernel_source_sha() else None
         except (OSError, ValueError):
             traffic, nc = None, {}
     # the issue ceiling the kernel actually runs into: warp
