@@ -2085,9 +2085,10 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) trave
         float alo[3], ahi[3], blo[3], bhi[3];
         words_to_float<FAST>(p.A, CA, alo, ahi);
         words_to_float<FAST>(p.B, CB, blo, bhi);
-        if (smem_boxes(MODE)) {
+        if (smem_boxes(MODE) && !FAST) {
           // park the child boxes in shared memory across the tests: under
-          // register pressure the compiler spills them to local memory
+          // register pressure the compiler spills them to local memory (the
+          // FAST distance kernel has the registers: 165, no spills, -1 %)
           #pragma unroll
           for (int q = 0; q < 6; ++q) {
             c.scr[q * 32 + c.lane] = (uint32_t)CA[q];
@@ -2208,7 +2209,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) trave
         if (push) {
           const int s2 = top + pos;
           CBVH_CHECK(p, s2 < kStack);
-          if (smem_boxes(MODE)) {
+          if (smem_boxes(MODE) && !FAST) {
             #pragma unroll
             for (int q = 0; q < 6; ++q) {
               CA[q] = (int32_t)c.scr[q * 32 + c.lane];
