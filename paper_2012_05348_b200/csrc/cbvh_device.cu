@@ -234,14 +234,19 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 // ---------------------------------------------------------------- decode
 
-// FAST (template parameter of the decode helpers and of traverse_kernel): the
-// default blob format — delta layout, b = 8 in 8-bit fields, codes not
-// zero-suppressed — as compile-time constants, so the per-child format
-// branches (and their constant loads) disappear from the production kernel;
-// every other format takes the generic instantiation.
-template <bool FAST = false>
+// FAST (template parameter of the decode helpers and of traverse_kernel): a
+// blob format as compile-time constants, so the per-child format branches (and
+// their constant loads) disappear from the kernel — 1: the default format
+// (delta layout, b = 8 in 8-bit fields, codes not zero-suppressed), 2 / 3: the
+// absolute binary16 / fp32 layouts of the paper's half-vs-float comparison
+// (§III.A); 0: any format, decided at run time (the generic instantiation).
+template <int FAST>
+__device__ __forceinline__ int fast_layout(const DevTree& T) {
+  return FAST == 0 ? T.layout : FAST == 1 ? CBVH_LAYOUT_DELTA : FAST == 2 ? CBVH_LAYOUT_FP16 : CBVH_LAYOUT_FP32;
+}
+template <int FAST = 0>
 __device__ __forceinline__ void load_codes(const DevTree& T, uint32_t node, uint32_t q[6]) {
-  if (FAST || T.width == 8) {
+  if (FAST == 1 || T.width == 8) {
     const unsigned short* p = reinterpret_cast<const unsigned short*>(T.codes + 6ull * node);
     uint32_t a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
     q[0] = a & 255u; q[1] = a >> 8; q[2] = b & 255u; q[3] = b >> 8; q[4] = c & 255u; q[5] = c >> 8;
@@ -326,20 +331,21 @@ __device__ __noinline__ uint3 load_codes_zs_global(const uint8_t* codes, const u
 // A node's box travels as 6 words: lattice ints (DELTA) or fp32 bits
 // (FP16 / FP32, absolute).  The child box comes from the parent's words
 // (DELTA: predictor-corrector decode) or straight from the record.
-template <bool FAST = false>
+template <int FAST = 0>
 __device__ __forceinline__ void fetch_child_box(const DevTree& T, uint32_t node, const int32_t P[6], int32_t C[6]) {
-  if (FAST || T.layout == CBVH_LAYOUT_DELTA) {
+  const int layout = fast_layout<FAST>(T);
+  if (layout == CBVH_LAYOUT_DELTA) {
     uint32_t q[6];
     // (zero-suppressed blobs: an out-of-line call, so the common path keeps
     // its registers and code layout; CBVH_ZS=0 builds without the branch)
-    if (!FAST && CBVH_ZS && T.zoff) {
+    if (FAST == 0 && CBVH_ZS && T.zoff) {
       const uint3 z = load_codes_zs_global(T.codes, T.zoff, T.tlog, T.width, node);
       q[0] = z.x & 0xffffu; q[1] = z.x >> 16; q[2] = z.y & 0xffffu; q[3] = z.y >> 16; q[4] = z.z & 0xffffu; q[5] = z.z >> 16;
     } else {
       load_codes<FAST>(T, node, q);
     }
-    decode_child(P, q, FAST ? 8 : T.bits, C);
-  } else if (T.layout == CBVH_LAYOUT_FP16) {
+    decode_child(P, q, FAST == 1 ? 8 : T.bits, C);
+  } else if (layout == CBVH_LAYOUT_FP16) {
     // binary16 descriptors (§III.A): widened exactly to fp32
     const uint32_t* w = reinterpret_cast<const uint32_t*>(T.codes + 12ull * node);
     const uint32_t a = __ldg(w), b = __ldg(w + 1), c = __ldg(w + 2);
@@ -354,9 +360,9 @@ __device__ __forceinline__ void fetch_child_box(const DevTree& T, uint32_t node,
   }
 }
 
-template <bool FAST = false>
+template <int FAST = 0>
 __device__ __forceinline__ void words_to_float(const DevTree& T, const int32_t C[6], float lo[3], float hi[3]) {
-  if (FAST || T.layout == CBVH_LAYOUT_DELTA) {
+  if (fast_layout<FAST>(T) == CBVH_LAYOUT_DELTA) {
     to_float_box(T, C, lo, hi);
   } else {
     #pragma unroll
@@ -365,9 +371,9 @@ __device__ __forceinline__ void words_to_float(const DevTree& T, const int32_t C
 }
 
 // sum of the box's extents (the larger-first descent rule's size measure)
-template <bool FAST = false>
+template <int FAST = 0>
 __device__ __forceinline__ float words_extent(const DevTree& T, const int32_t C[6]) {
-  if (FAST || T.layout == CBVH_LAYOUT_DELTA)
+  if (fast_layout<FAST>(T) == CBVH_LAYOUT_DELTA)
     return (float)((C[3] - C[0]) + (C[4] - C[1]) + (C[5] - C[2])) * T.cell;
   return (__int_as_float(C[3]) - __int_as_float(C[0])) + (__int_as_float(C[4]) - __int_as_float(C[1])) +
          (__int_as_float(C[5]) - __int_as_float(C[2]));
@@ -1116,7 +1122,7 @@ __device__ __forceinline__ int pair_count(uint32_t pw, uint32_t ta, uint32_t tb)
 // both when both are internal; the LARGER rule descends only the node with the
 // larger box (sum of extents, A-local vs world — rotation-invariant up to
 // sqrt 3), which visits the same leaf pairs (reading R15).
-template <bool FAST = false>
+template <int FAST = 0>
 __device__ __forceinline__ uint32_t descent_flags(int rule, uint32_t ta, uint32_t tb, const int32_t CA[6],
                                                   const int32_t CB[6], const DevTree& TA, const DevTree& TB) {
   const bool ai = !(ta & kLeafBit), bi = !(tb & kLeafBit);
@@ -1526,7 +1532,7 @@ __device__ __forceinline__ void exact_batch(const Params& p, const WarpCtx c, in
 // expensive tests 32 at a time, so Möller / the distance code run with full
 // lanes instead of the ~20-30 % the culls leave.  Returns the number of
 // triangle-pair tests (stats).
-template <int MODE, bool STATS, bool FAST = false>
+template <int MODE, bool STATS, int FAST = 0>
 __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx c, int nleaf,
                                                  unsigned long long* exact) {
   unsigned tests = 0;
@@ -1758,12 +1764,12 @@ __device__ __noinline__ bool dump_items(const Params& p, const WarpCtx c, int to
 #ifndef CBVH_MIN_BLOCKS_FAST
 #define CBVH_MIN_BLOCKS_FAST 7
 #endif
-__host__ __device__ constexpr int min_blocks(int mode, int kx, bool fast = false) {
+__host__ __device__ constexpr int min_blocks(int mode, int kx, int fast = 0) {
   return kx == 0 ? (mode == 0 ? (fast ? CBVH_MIN_BLOCKS_FAST : CBVH_MIN_BLOCKS) : CBVH_MIN_BLOCKS_DIST)
                  : (mode == 0 ? (kx >= 10 ? 3 : 4) : 3);
 }
 
-template <int MODE, bool STATS, int KX, bool STAGE, bool FAST>
+template <int MODE, bool STATS, int KX, bool STAGE, int FAST>
 __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) traverse_kernel(const __grid_constant__ Params p) {
   constexpr int NF = nfields(KX);
   extern __shared__ uint32_t smem[];
@@ -2374,7 +2380,7 @@ constexpr int kMaxDevices = 64;
 
 // Grid of the persistent traversal kernel: SMs x resident CTAs at `smem`
 // bytes of dynamic shared memory per CTA.
-template <int MODE, bool STATS, int KX, bool STAGE, bool FAST = false>
+template <int MODE, bool STATS, int KX, bool STAGE, int FAST = 0>
 static int shape_for(LaunchShape* s, size_t smem) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -2418,10 +2424,12 @@ static int max_warps_kx(int mode) {
   if (rc) return -1;
   int w = a.warps > b.warps ? a.warps : b.warps;
   if constexpr (KX == 0) {
-    LaunchShape f{};
-    rc = mode == 0 ? shape_for<0, false, 0, false, true>(&f, smem_bytes(0, 0)) : shape_for<1, false, 0, false, true>(&f, smem_bytes(1, 0));
+    LaunchShape f[3] = {};
+    rc = mode == 0 ? shape_for<0, false, 0, false, 1>(&f[0], smem_bytes(0, 0)) : shape_for<1, false, 0, false, 1>(&f[0], smem_bytes(1, 0));
+    if (!rc) rc = mode == 0 ? shape_for<0, false, 0, false, 2>(&f[1], smem_bytes(0, 0)) : shape_for<1, false, 0, false, 2>(&f[1], smem_bytes(1, 0));
+    if (!rc) rc = mode == 0 ? shape_for<0, false, 0, false, 3>(&f[2], smem_bytes(0, 0)) : shape_for<1, false, 0, false, 3>(&f[2], smem_bytes(1, 0));
     if (rc) return -1;
-    w = f.warps > w ? f.warps : w;
+    for (const LaunchShape& x : f) w = x.warps > w ? x.warps : w;
   }
   return w;
 }
@@ -2589,13 +2597,20 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   // the default blob format and query options run the FAST instantiation
   // (format constants folded at compile time); everything else the generic one
   auto plain = [](const DevTree& T) { return T.layout == CBVH_LAYOUT_DELTA && T.width == 8 && T.bits == 8 && !T.zoff; };
-  const bool fast = !STATS && KX == 0 && !stage && plain(p.A) && plain(p.B) && descent == CBVH_DESCENT_LARGER &&
-                    !(MODE == 0 && early_exit) && fast_enabled();
+  int fast = 0;
+  if (!STATS && KX == 0 && !stage && descent == CBVH_DESCENT_LARGER && !(MODE == 0 && early_exit) && fast_enabled()) {
+    if (plain(p.A) && plain(p.B)) fast = 1;
+    else if (p.A.layout == CBVH_LAYOUT_FP16 && p.B.layout == CBVH_LAYOUT_FP16) fast = 2;
+    else if (p.A.layout == CBVH_LAYOUT_FP32 && p.B.layout == CBVH_LAYOUT_FP32) fast = 3;
+  }
   LaunchShape s;
   int rc;
   if constexpr (KX == 0 && !STATS) {
     rc = stage ? shape_for<MODE, STATS, KX, true>(&s, smem)
-               : (fast ? shape_for<MODE, STATS, KX, false, true>(&s, smem) : shape_for<MODE, STATS, KX, false>(&s, smem));
+         : fast == 1 ? shape_for<MODE, STATS, KX, false, 1>(&s, smem)
+         : fast == 2 ? shape_for<MODE, STATS, KX, false, 2>(&s, smem)
+         : fast == 3 ? shape_for<MODE, STATS, KX, false, 3>(&s, smem)
+                     : shape_for<MODE, STATS, KX, false>(&s, smem);
   } else if constexpr (KX == 0) {
     rc = stage ? shape_for<MODE, STATS, KX, true>(&s, smem) : shape_for<MODE, STATS, KX, false>(&s, smem);
   } else {
@@ -2652,14 +2667,16 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
     p.cont_in = (ph & 1) ? cont0 : cont1;   // phase ph reads what ph - 1 wrote
     p.cont_out = (ph & 1) ? cont1 : cont0;
     if constexpr (KX == 0 && !STATS) {
-      if (stage) e = launch_after(traverse_kernel<MODE, STATS, KX, true, false>, s.blocks, kWarps * 32, smem, st, p);
-      else if (fast) e = launch_after(traverse_kernel<MODE, STATS, KX, false, true>, s.blocks, kWarps * 32, smem, st, p);
-      else e = launch_after(traverse_kernel<MODE, STATS, KX, false, false>, s.blocks, kWarps * 32, smem, st, p);
+      if (stage) e = launch_after(traverse_kernel<MODE, STATS, KX, true, 0>, s.blocks, kWarps * 32, smem, st, p);
+      else if (fast == 1) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 1>, s.blocks, kWarps * 32, smem, st, p);
+      else if (fast == 2) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 2>, s.blocks, kWarps * 32, smem, st, p);
+      else if (fast == 3) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 3>, s.blocks, kWarps * 32, smem, st, p);
+      else e = launch_after(traverse_kernel<MODE, STATS, KX, false, 0>, s.blocks, kWarps * 32, smem, st, p);
     } else if constexpr (KX == 0) {
-      if (stage) e = launch_after(traverse_kernel<MODE, STATS, KX, true, false>, s.blocks, kWarps * 32, smem, st, p);
-      else e = launch_after(traverse_kernel<MODE, STATS, KX, false, false>, s.blocks, kWarps * 32, smem, st, p);
+      if (stage) e = launch_after(traverse_kernel<MODE, STATS, KX, true, 0>, s.blocks, kWarps * 32, smem, st, p);
+      else e = launch_after(traverse_kernel<MODE, STATS, KX, false, 0>, s.blocks, kWarps * 32, smem, st, p);
     } else {
-      e = launch_after(traverse_kernel<MODE, STATS, KX, false, false>, s.blocks, kWarps * 32, smem, st, p);
+      e = launch_after(traverse_kernel<MODE, STATS, KX, false, 0>, s.blocks, kWarps * 32, smem, st, p);
     }
     g_launches++;
     if (e != cudaSuccess) return cuda_fail(e, "traverse_kernel launch");
