@@ -1532,7 +1532,7 @@ __device__ __forceinline__ void exact_batch(const Params& p, const WarpCtx c, in
 // expensive tests 32 at a time, so Möller / the distance code run with full
 // lanes instead of the ~20-30 % the culls leave.  Returns the number of
 // triangle-pair tests (stats).
-template <int MODE, bool STATS, int FAST = 0>
+template <int MODE, bool STATS, int FAST = 0, bool EE = false>
 __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx c, int nleaf,
                                                  unsigned long long* exact) {
   unsigned tests = 0;
@@ -1549,7 +1549,7 @@ __device__ CBVH_DRAIN_ATTR unsigned drain_leaves(const Params& p, const WarpCtx 
       mk = c.lq[3 * kLeafQ + head + c.lane];
       n = (int)((mk >> 8) & 7u) * (int)((mk >> 19) & 7u);  // only triangles the box filters kept
       // early exit: a pose that already has a hit needs no more tests
-      if (MODE == 0 && !FAST && p.early_exit && __ldcg(&p.hit[pose])) n = 0;
+      if (MODE == 0 && (FAST ? EE : p.early_exit != 0) && __ldcg(&p.hit[pose])) n = 0;
       // distance: a leaf pair whose box bound no longer beats the pose's best
       // distance (tightened since it was queued) is skipped
       if (MODE == 1 && __uint_as_float(c.lq[4 * kLeafQ + head + c.lane]) >= __uint_as_float(__ldcg(&p.dist_bits[pose])))
@@ -1769,7 +1769,7 @@ __host__ __device__ constexpr int min_blocks(int mode, int kx, int fast = 0) {
                  : (mode == 0 ? (kx >= 10 ? 3 : 4) : 3);
 }
 
-template <int MODE, bool STATS, int KX, bool STAGE, int FAST>
+template <int MODE, bool STATS, int KX, bool STAGE, int FAST, bool EE = false>
 __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) traverse_kernel(const __grid_constant__ Params p) {
   constexpr int NF = nfields(KX);
   extern __shared__ uint32_t smem[];
@@ -1777,7 +1777,8 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) trave
   grid_dependency_wait();  // the previous phase's continuation items, init_kernel's outputs and control block
   grid_launch_dependents();
   static_assert(!FAST || (!STATS && KX == 0 && !STAGE), "FAST is the default-format production kernel");
-  const int early_exit = FAST ? 0 : p.early_exit;
+  static_assert(!EE || (FAST == 1 && MODE == 0), "EE: the hit-only FAST collide kernel");
+  const int early_exit = FAST ? (EE ? 1 : 0) : p.early_exit;  // (FAST: the option is the template parameter EE)
   const int descent = FAST ? CBVH_DESCENT_LARGER : p.descent;
   WarpCtx c;
   c.lane = threadIdx.x & 31;
@@ -1864,7 +1865,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) trave
           if (root_leafpair) nleaf += k; else top += k;
           __syncwarp();
           if (nleaf > kLeafQ - 32) {
-            s_tri += drain_leaves<MODE, STATS, FAST>(p, c, nleaf, &s_exact);
+            s_tri += drain_leaves<MODE, STATS, FAST, EE>(p, c, nleaf, &s_exact);
             nleaf = 0;
           }
         }
@@ -1920,7 +1921,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) trave
     // ---- bounded work after the input ran out: hand the rest to the next phase
     if (!poses_left && p.budget >= 0 && ++after > p.budget) {
       if (nleaf > 0) {
-        s_tri += drain_leaves<MODE, STATS, FAST>(p, c, nleaf, &s_exact);
+        s_tri += drain_leaves<MODE, STATS, FAST, EE>(p, c, nleaf, &s_exact);
         nleaf = 0;
       }
       if (dump_items<NF>(p, c, top, spill_top)) {
@@ -2262,7 +2263,7 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) trave
       // the half-empty rounds cost more than the pruning gains)
       if (nleaf > kLeafQ - 32 || (MODE == 1 && nleaf >= CBVH_DIST_DRAIN) ||
           (MODE == 0 && early_exit && nleaf >= CBVH_EE_DRAIN)) {
-        s_tri += drain_leaves<MODE, STATS, FAST>(p, c, nleaf, &s_exact);
+        s_tri += drain_leaves<MODE, STATS, FAST, EE>(p, c, nleaf, &s_exact);
         nleaf = 0;
       }
     }
@@ -2274,11 +2275,11 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) trave
       top -= 1;
     }
     if (MODE == 1 && nleaf > 0 && top == 0) {
-      s_tri += drain_leaves<MODE, STATS, FAST>(p, c, nleaf, &s_exact);
+      s_tri += drain_leaves<MODE, STATS, FAST, EE>(p, c, nleaf, &s_exact);
       nleaf = 0;
     }
   }
-  if (nleaf > 0) s_tri += drain_leaves<MODE, STATS, FAST>(p, c, nleaf, &s_exact);
+  if (nleaf > 0) s_tri += drain_leaves<MODE, STATS, FAST, EE>(p, c, nleaf, &s_exact);
   if (STATS && c.lane == 0) atomicMax(&p.ctl->t_end, globaltimer_ns());
   if (STATS) {
     unsigned long long d = s_dec, r = s_rec, lb = s_lbytes, ex = s_exact;
@@ -2380,7 +2381,7 @@ constexpr int kMaxDevices = 64;
 
 // Grid of the persistent traversal kernel: SMs x resident CTAs at `smem`
 // bytes of dynamic shared memory per CTA.
-template <int MODE, bool STATS, int KX, bool STAGE, int FAST = 0>
+template <int MODE, bool STATS, int KX, bool STAGE, int FAST = 0, bool EE = false>
 static int shape_for(LaunchShape* s, size_t smem) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -2398,10 +2399,10 @@ static int shape_for(LaunchShape* s, size_t smem) {
     e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
     if (smem > (size_t)optin) return set_error(CBVH_EINVAL, "shared memory of the staged kernel exceeds the device limit");
-    e = cudaFuncSetAttribute(traverse_kernel<MODE, STATS, KX, STAGE, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(traverse_kernel<MODE, STATS, KX, STAGE, FAST, EE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              STAGE ? optin : (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel<MODE, STATS, KX, STAGE, FAST>, kWarps * 32,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, traverse_kernel<MODE, STATS, KX, STAGE, FAST, EE>, kWarps * 32,
                                                       smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
@@ -2424,7 +2425,8 @@ static int max_warps_kx(int mode) {
   if (rc) return -1;
   int w = a.warps > b.warps ? a.warps : b.warps;
   if constexpr (KX == 0) {
-    LaunchShape f[3] = {};
+    LaunchShape f[4] = {};
+    if (mode == 0 && shape_for<0, false, 0, false, 1, true>(&f[3], smem_bytes(0, 0))) return -1;
     rc = mode == 0 ? shape_for<0, false, 0, false, 1>(&f[0], smem_bytes(0, 0)) : shape_for<1, false, 0, false, 1>(&f[0], smem_bytes(1, 0));
     if (!rc) rc = mode == 0 ? shape_for<0, false, 0, false, 2>(&f[1], smem_bytes(0, 0)) : shape_for<1, false, 0, false, 2>(&f[1], smem_bytes(1, 0));
     if (!rc) rc = mode == 0 ? shape_for<0, false, 0, false, 3>(&f[2], smem_bytes(0, 0)) : shape_for<1, false, 0, false, 3>(&f[2], smem_bytes(1, 0));
@@ -2598,8 +2600,10 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   // (format constants folded at compile time); everything else the generic one
   auto plain = [](const DevTree& T) { return T.layout == CBVH_LAYOUT_DELTA && T.width == 8 && T.bits == 8 && !T.zoff; };
   int fast = 0;
-  if (!STATS && KX == 0 && !stage && descent == CBVH_DESCENT_LARGER && !(MODE == 0 && early_exit) && fast_enabled()) {
-    if (plain(p.A) && plain(p.B)) fast = 1;
+  const bool ee = MODE == 0 && early_exit;
+  if (!STATS && KX == 0 && !stage && descent == CBVH_DESCENT_LARGER && fast_enabled()) {
+    if (plain(p.A) && plain(p.B)) fast = 1;  // (also hit-only collide: the EE instantiation)
+    else if (ee) fast = 0;
     else if (p.A.layout == CBVH_LAYOUT_FP16 && p.B.layout == CBVH_LAYOUT_FP16) fast = 2;
     else if (p.A.layout == CBVH_LAYOUT_FP32 && p.B.layout == CBVH_LAYOUT_FP32) fast = 3;
   }
@@ -2607,6 +2611,7 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
   int rc;
   if constexpr (KX == 0 && !STATS) {
     rc = stage ? shape_for<MODE, STATS, KX, true>(&s, smem)
+         : (fast == 1 && ee) ? shape_for<0, STATS, KX, false, 1, true>(&s, smem)
          : fast == 1 ? shape_for<MODE, STATS, KX, false, 1>(&s, smem)
          : fast == 2 ? shape_for<MODE, STATS, KX, false, 2>(&s, smem)
          : fast == 3 ? shape_for<MODE, STATS, KX, false, 3>(&s, smem)
@@ -2668,6 +2673,7 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
     p.cont_out = (ph & 1) ? cont1 : cont0;
     if constexpr (KX == 0 && !STATS) {
       if (stage) e = launch_after(traverse_kernel<MODE, STATS, KX, true, 0>, s.blocks, kWarps * 32, smem, st, p);
+      else if (fast == 1 && ee) e = launch_after(traverse_kernel<0, STATS, KX, false, 1, true>, s.blocks, kWarps * 32, smem, st, p);
       else if (fast == 1) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 1>, s.blocks, kWarps * 32, smem, st, p);
       else if (fast == 2) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 2>, s.blocks, kWarps * 32, smem, st, p);
       else if (fast == 3) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 3>, s.blocks, kWarps * 32, smem, st, p);

@@ -568,7 +568,7 @@ def test_production_kernels_do_not_spill(tmp_path):
     lines = out.splitlines()
     for mode in (0, 1):
         for fast in (0, 1, 2, 3):  # the generic instantiation and the FAST ones (delta b = 8, fp16, fp32)
-            tag = f"_ZN4cbvh15traverse_kernelILi{mode}ELb0ELi0ELb0ELi{fast}EEEvNS_6ParamsE"
+            tag = f"_ZN4cbvh15traverse_kernelILi{mode}ELb0ELi0ELb0ELi{fast}ELb0EEEvNS_6ParamsE"
             i = next(k for k, l in enumerate(lines) if "Function properties for " + tag in l)
             if (mode, fast) == (0, 1):
                 # the default-format collide kernel runs 7 CTAs / SM at 72 registers:
