@@ -240,17 +240,24 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // (delta layout, b = 8 in 8-bit fields, codes not zero-suppressed), 2 / 3: the
 // absolute binary16 / fp32 layouts of the paper's half-vs-float comparison
 // (§III.A); 0: any format, decided at run time (the generic instantiation).
+// 4 / 5: the delta layout in 4- / 16-bit fields (any b up to the field width;
+// BJ config 3 sweeps b = 4, 8, 16), not zero-suppressed.
 template <int FAST>
 __device__ __forceinline__ int fast_layout(const DevTree& T) {
-  return FAST == 0 ? T.layout : FAST == 1 ? CBVH_LAYOUT_DELTA : FAST == 2 ? CBVH_LAYOUT_FP16 : CBVH_LAYOUT_FP32;
+  return FAST == 0 ? T.layout : FAST == 2 ? CBVH_LAYOUT_FP16 : FAST == 3 ? CBVH_LAYOUT_FP32 : CBVH_LAYOUT_DELTA;
+}
+template <int FAST>
+__device__ __forceinline__ int fast_width(const DevTree& T) {
+  return FAST == 1 ? 8 : FAST == 4 ? 4 : FAST == 5 ? 16 : T.width;
 }
 template <int FAST = 0>
 __device__ __forceinline__ void load_codes(const DevTree& T, uint32_t node, uint32_t q[6]) {
-  if (FAST == 1 || T.width == 8) {
+  const int width = fast_width<FAST>(T);
+  if (width == 8) {
     const unsigned short* p = reinterpret_cast<const unsigned short*>(T.codes + 6ull * node);
     uint32_t a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
     q[0] = a & 255u; q[1] = a >> 8; q[2] = b & 255u; q[3] = b >> 8; q[4] = c & 255u; q[5] = c >> 8;
-  } else if (T.width == 16) {
+  } else if (width == 16) {
     const uint32_t* p = reinterpret_cast<const uint32_t*>(T.codes + 12ull * node);
     uint32_t a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
     q[0] = a & 0xffffu; q[1] = a >> 16; q[2] = b & 0xffffu; q[3] = b >> 16; q[4] = c & 0xffffu; q[5] = c >> 16;
@@ -344,7 +351,7 @@ __device__ __forceinline__ void fetch_child_box(const DevTree& T, uint32_t node,
     } else {
       load_codes<FAST>(T, node, q);
     }
-    decode_child(P, q, FAST == 1 ? 8 : T.bits, C);
+    decode_child(P, q, FAST == 1 ? 8 : T.bits, C);  // (FAST 4 / 5: b at run time, one constant load)
   } else if (layout == CBVH_LAYOUT_FP16) {
     // binary16 descriptors (§III.A): widened exactly to fp32
     const uint32_t* w = reinterpret_cast<const uint32_t*>(T.codes + 12ull * node);
@@ -2425,7 +2432,10 @@ static int max_warps_kx(int mode) {
   if (rc) return -1;
   int w = a.warps > b.warps ? a.warps : b.warps;
   if constexpr (KX == 0) {
-    LaunchShape f[4] = {};
+    LaunchShape f[6] = {};
+    rc = mode == 0 ? shape_for<0, false, 0, false, 4>(&f[4], smem_bytes(0, 0)) : shape_for<1, false, 0, false, 4>(&f[4], smem_bytes(1, 0));
+    if (!rc) rc = mode == 0 ? shape_for<0, false, 0, false, 5>(&f[5], smem_bytes(0, 0)) : shape_for<1, false, 0, false, 5>(&f[5], smem_bytes(1, 0));
+    if (rc) return -1;
     if (mode == 0 && shape_for<0, false, 0, false, 1, true>(&f[3], smem_bytes(0, 0))) return -1;
     rc = mode == 0 ? shape_for<0, false, 0, false, 1>(&f[0], smem_bytes(0, 0)) : shape_for<1, false, 0, false, 1>(&f[0], smem_bytes(1, 0));
     if (!rc) rc = mode == 0 ? shape_for<0, false, 0, false, 2>(&f[1], smem_bytes(0, 0)) : shape_for<1, false, 0, false, 2>(&f[1], smem_bytes(1, 0));
@@ -2598,12 +2608,14 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
                       (stage ? (size_t)kWarps * (kStageTagWords + kStageSlots * p.stage_slot_words) * sizeof(uint32_t) : 0);
   // the default blob format and query options run the FAST instantiation
   // (format constants folded at compile time); everything else the generic one
-  auto plain = [](const DevTree& T) { return T.layout == CBVH_LAYOUT_DELTA && T.width == 8 && T.bits == 8 && !T.zoff; };
+  auto plain = [](const DevTree& T, int w) { return T.layout == CBVH_LAYOUT_DELTA && T.width == w && !T.zoff; };
   int fast = 0;
   const bool ee = MODE == 0 && early_exit;
   if (!STATS && KX == 0 && !stage && descent == CBVH_DESCENT_LARGER && fast_enabled()) {
-    if (plain(p.A) && plain(p.B)) fast = 1;  // (also hit-only collide: the EE instantiation)
+    if (plain(p.A, 8) && plain(p.B, 8) && p.A.bits == 8 && p.B.bits == 8) fast = 1;  // (also hit-only collide: the EE instantiation)
     else if (ee) fast = 0;
+    else if (plain(p.A, 4) && plain(p.B, 4)) fast = 4;
+    else if (plain(p.A, 16) && plain(p.B, 16)) fast = 5;
     else if (p.A.layout == CBVH_LAYOUT_FP16 && p.B.layout == CBVH_LAYOUT_FP16) fast = 2;
     else if (p.A.layout == CBVH_LAYOUT_FP32 && p.B.layout == CBVH_LAYOUT_FP32) fast = 3;
   }
@@ -2615,6 +2627,8 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
          : fast == 1 ? shape_for<MODE, STATS, KX, false, 1>(&s, smem)
          : fast == 2 ? shape_for<MODE, STATS, KX, false, 2>(&s, smem)
          : fast == 3 ? shape_for<MODE, STATS, KX, false, 3>(&s, smem)
+         : fast == 4 ? shape_for<MODE, STATS, KX, false, 4>(&s, smem)
+         : fast == 5 ? shape_for<MODE, STATS, KX, false, 5>(&s, smem)
                      : shape_for<MODE, STATS, KX, false>(&s, smem);
   } else if constexpr (KX == 0) {
     rc = stage ? shape_for<MODE, STATS, KX, true>(&s, smem) : shape_for<MODE, STATS, KX, false>(&s, smem);
@@ -2677,6 +2691,8 @@ static int launch_kx(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses,
       else if (fast == 1) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 1>, s.blocks, kWarps * 32, smem, st, p);
       else if (fast == 2) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 2>, s.blocks, kWarps * 32, smem, st, p);
       else if (fast == 3) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 3>, s.blocks, kWarps * 32, smem, st, p);
+      else if (fast == 4) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 4>, s.blocks, kWarps * 32, smem, st, p);
+      else if (fast == 5) e = launch_after(traverse_kernel<MODE, STATS, KX, false, 5>, s.blocks, kWarps * 32, smem, st, p);
       else e = launch_after(traverse_kernel<MODE, STATS, KX, false, 0>, s.blocks, kWarps * 32, smem, st, p);
     } else if constexpr (KX == 0) {
       if (stage) e = launch_after(traverse_kernel<MODE, STATS, KX, true, 0>, s.blocks, kWarps * 32, smem, st, p);
