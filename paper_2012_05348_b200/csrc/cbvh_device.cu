@@ -736,7 +736,13 @@ __device__ __forceinline__ Tri rec_tri(const TriRec& r) {
 // Only the triangles in `todo` are tested: a triangle the parent box missed
 // cannot touch the child box (child ⊆ parent, same eps), so the mask an item
 // inherits from its parent's refinement is a valid starting set.
-template <int DIR>
+// PF: the next triangle's record is fetched while the current one is tested —
+// worth 6 % at 5 CTAs / SM (round 1: 95 -> 89 ms), but at the FAST kernels' 7
+// CTAs the other warps hide the latency and the 12 registers of the
+// prefetched record cost more: without it config 5 37.2 -> 36.3 ms, config 3
+// 41.9 -> 41.1, config 2 3.56 -> 3.43 and no spills at 72 registers
+// (profiles/round2_ab_prefetch.txt).
+template <int DIR, bool PF = true>
 __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float lo[3], const float hi[3],
                                                const float* tris, uint32_t leaf, float eps, uint32_t todo) {
   const uint32_t first = leaf & 0x1FFFFFFFu;
@@ -754,16 +760,18 @@ __device__ CBVH_FILTER_ATTR uint32_t box_hits_leaf(const PoseF& P, const float l
   if (todo == 0u) return 0u;
   uint32_t qn = (uint32_t)__ffs(todo) - 1u;
   todo &= todo - 1u;
-  TriRec next = load_rec(tris, first + qn);
+  TriRec next;
+  if (PF) next = load_rec(tris, first + qn);
   #pragma unroll 1
   while (true) {
-    const TriRec cur = next;
     const uint32_t q = qn;
+    TriRec cur;
+    if (PF) cur = next; else cur = load_rec(tris, first + q);
     const bool more = todo != 0u;
     if (more) {
       qn = (uint32_t)__ffs(todo) - 1u;
       todo &= todo - 1u;
-      next = load_rec(tris, first + qn);
+      if (PF) next = load_rec(tris, first + qn);
     }
     const Tri L = rec_tri(cur);
     Tri W;
@@ -2146,11 +2154,11 @@ __global__ void __launch_bounds__(kWarps * 32, min_blocks(MODE, KX, FAST)) trave
           const bool doB = lbf;
 #endif
           if (surv && doB) {
-            mskB = box_hits_leaf<0>(P, alo, ahi, p.B.tris, ctb, eps, mskB);
+            mskB = box_hits_leaf<0, FAST == 0>(P, alo, ahi, p.B.tris, ctb, eps, mskB);
             surv = mskB != 0u;
           }
           if (surv && doA) {
-            mskA = box_hits_leaf<1>(P, blo, bhi, p.A.tris, cta, eps, mskA);
+            mskA = box_hits_leaf<1, FAST == 0>(P, blo, bhi, p.A.tris, cta, eps, mskA);
             surv = mskA != 0u;
           }
         } else {

@@ -570,11 +570,4 @@ def test_production_kernels_do_not_spill(tmp_path):
         for fast in (0, 1, 2, 3, 4, 5):  # generic, and FAST: delta b = 8, fp16, fp32, delta in 4- / 16-bit fields
             tag = f"_ZN4cbvh15traverse_kernelILi{mode}ELb0ELi0ELb0ELi{fast}ELb0EEEvNS_6ParamsE"
             i = next(k for k, l in enumerate(lines) if "Function properties for " + tag in l)
-            if mode == 0 and fast in (1, 4, 5):
-                # the delta-format FAST collide kernels run 7 CTAs / SM at 72 registers:
-                # at most a few bytes of spills (measured faster than 6 CTAs without any)
-                import re
-                st, ld = map(int, re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", lines[i + 1]).groups())
-                assert st <= 32 and ld <= 32, lines[i + 1]
-            else:
-                assert "0 bytes spill stores, 0 bytes spill loads" in lines[i + 1], lines[i + 1]
+            assert "0 bytes spill stores, 0 bytes spill loads" in lines[i + 1], lines[i + 1]
