@@ -762,3 +762,23 @@ def test_warp_dive_arities(M, cfg1, Bf, kdop):
     P = w.poses[:192]
     d64, _ = O.distance(tA, tB, P)
     check_distance(run_distance(M, A, B, P), d64, delta, f"warp dive B={Bf} k={kdop}")
+
+
+def test_fast_and_generic_kernels_agree_full_size(M):
+    # default blobs run the FAST instantiations (format and options folded at
+    # compile time, 7 CTAs / SM); the stats variant runs the generic kernel on
+    # the same blobs: identical counts on the whole config-5 batch, identical
+    # hit flags for the hit-only query, bit-identical distances on config 4
+    w = G.make_config(5)
+    A, B = build(M, w.A, w.branching, w.bits, w.treelet), build(M, w.B, w.branching, w.bits, w.treelet)
+    hit_f, cnt_f = run_collide(M, A, B, w.poses)
+    hit_g, cnt_g, st = run_collide(M, A, B, w.poses, stats=True)
+    assert np.array_equal(cnt_f, cnt_g) and np.array_equal(hit_f, hit_g)
+    assert st["bv_tests"] > 8e8
+    hit_e, _ = run_collide(M, A, B, w.poses, early_exit=True)
+    assert np.array_equal(hit_e, hit_f)
+    w4 = G.make_config(4, num_poses=16384)
+    A4, B4 = build(M, w4.A, w4.branching, w4.bits, w4.treelet), build(M, w4.B, w4.branching, w4.bits, w4.treelet)
+    d_f = run_distance(M, A4, B4, w4.poses)
+    d_g, _ = run_distance(M, A4, B4, w4.poses, stats=True)
+    assert np.array_equal(d_f, d_g)
