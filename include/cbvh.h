@@ -165,7 +165,14 @@ size_t cbvh_workspace_bytes(const cbvh_bvh* A, const cbvh_bvh* B, int64_t N, int
  *   d_ws:         device workspace of ws_bytes >= cbvh_workspace_bytes(...)
  *   stream:       cudaStream_t (as void*), 0 = legacy default stream
  * N = 0 is a no-op.  Errors (synchronous): CBVH_EINVAL, CBVH_EWORKSPACE,
- * CBVH_ECUDA (launch failure).  Asynchronous: see cbvh_check. */
+ * CBVH_ECUDA (launch failure).  Asynchronous: see cbvh_check.
+ * Execution: init + 4-5 traversal phases on `stream`, chained with
+ * programmatic dependent launches (each kernel waits for its predecessor in
+ * the stream before touching its data; work queued on `stream` before or
+ * after the call is ordered as usual).  Blobs in the default format (delta
+ * layout, b = 8, not zero-suppressed) with default options — and the fp16 /
+ * fp32 layouts, 4- / 16-bit fields and the hit-only option — run kernels with
+ * the format compiled in; results do not depend on which kernel runs. */
 int collide_batch(const cbvh_bvh* A, const cbvh_bvh* B, const float* d_poses, int64_t N,
                   uint8_t* d_hit, uint32_t* d_pair_count, void* d_ws, size_t ws_bytes, void* stream);
 
