@@ -506,7 +506,11 @@ def run(args):
                          "kernel": "traverse_kernel<%s> (all phases)" % ("distance" if distance else "collide"),
                          "kernel_ms": 1e3 * kern_s,
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "peak_source": peaks["_source"] + " hbm_gbs (copy bandwidth)"},
+                         "peak_source": peaks["_source"] + " hbm_gbs (copy bandwidth)",
+                         "limiter": ("warp-issue slots, not memory: the hierarchy and most triangle records are "
+                                     "L1/L2-resident (DRAM traffic is a few % of the algorithmic bytes); see "
+                                     "roofline_issue" + (" (frac %.2f)" % issue["frac"] if issue else "")
+                                     + " and DESIGN.md §4.1")},
             "roofline_l2": ({"bound": "l2", "achieved": achieved, "peak": l2["l2_read_gbs"], "unit": "GB/s",
                             "frac": achieved / l2["l2_read_gbs"], "kernel": "traverse_kernel (all phases)",
                             "peak_source": l2["source"], "l2_bytes": l2["l2_bytes"],
