@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Latency of small batches (the launch- and dive-bound regime): median time of
 collide_batch / distance_batch over N poses of a config's meshes.
-    CBVH_LIB=... python tools/small_batch.py [config] [N ...]"""
+    CBVH_LIB=... python tools/small_batch.py [config] [N ...]      (MODES=collide,distance selects the queries)"""
 import os
 import statistics
 import sys
@@ -21,7 +21,7 @@ def main(cfg, sizes):
     B = M.build_compressed_bvh(w.B.vertices, w.B.triangles, w.branching, w.bits, w.treelet).to_device(dev)
     P = torch.from_numpy(w.poses).to(dev)
     st = torch.cuda.current_stream(dev)
-    for mode in ("collide", "distance"):
+    for mode in os.environ.get("MODES", "collide,distance").split(","):
         ws = M.Workspace(A, B, 1 if mode == "distance" else 0, dev)
         for n in sizes:
             Pn = P[:n].contiguous()
