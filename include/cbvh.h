@@ -166,7 +166,7 @@ size_t cbvh_workspace_bytes(const cbvh_bvh* A, const cbvh_bvh* B, int64_t N, int
  *   stream:       cudaStream_t (as void*), 0 = legacy default stream
  * N = 0 is a no-op.  Errors (synchronous): CBVH_EINVAL, CBVH_EWORKSPACE,
  * CBVH_ECUDA (launch failure).  Asynchronous: see cbvh_check.
- * Execution: init + 4-5 traversal phases on `stream`, chained with
+ * Execution: init + up to 8 traversal phases on `stream`, chained with
  * programmatic dependent launches (each kernel waits for its predecessor in
  * the stream before touching its data; work queued on `stream` before or
  * after the call is ordered as usual).  Blobs in the default format (delta

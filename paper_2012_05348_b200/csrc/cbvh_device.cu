@@ -2510,9 +2510,14 @@ static int phase_budgets(int* out, int64_t N) {
         if (*q == ',') ++q;
       }
     } else {
-      r.b[r.n++] = 32;
-      r.b[r.n++] = 32;
-      r.b[r.n++] = 64;
+      // seven bounded phases of 32 iterations, then the unbounded one: the
+      // last phase has no hand-over, so its longest chain is the call's tail
+      // (16k poses of config 5: 0.5 ms at 10 % SM activity behind 32, 32, 64);
+      // more, equally short phases leave it almost nothing, and a phase with
+      // nothing to do costs ~7 us (tools/ab_phases_full.sh, small_batch.py:
+      // config 5 at 16k / 131k / 1M poses -12 / -3 / -0.5 %, config 4 distance
+      // at 1,024 poses -16 %)
+      for (int k = 0; k < kMaxPhases - 1; ++k) r.b[r.n++] = 32;
     }
     return r;
   }();
